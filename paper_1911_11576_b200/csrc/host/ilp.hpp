@@ -1,0 +1,56 @@
+// Fusion-plan selection (paper §4.1): maximise sum_j X_j f(P_j) subject to
+// X_u + X_v <= 1 for overlapping patterns, iterated with cycle constraints
+// until the contracted graph is acyclic. Same API and same answers as the
+// reference's proj/include/stitch/ilp_solver.hpp: the optimum is the largest
+// "canonical" total (scores summed in ascending variable order) and ties go to
+// the lexicographically smallest index set. The search itself is ours: a
+// clique-cover bound (patterns sharing a graph node are mutually exclusive)
+// and witness-guided extraction replace the reference's additive bound, which
+// takes minutes on a few thousand candidates.
+#pragma once
+
+#include <vector>
+
+#include "ir.hpp"
+
+namespace stitch {
+
+struct PairConstraint {
+  int u = 0;
+  int v = 0;
+};
+
+struct CycleConstraint {
+  std::vector<int> pattern_indices;
+};
+
+struct IlpInstance {
+  int num_vars = 0;
+  std::vector<double> scores;
+  std::vector<PairConstraint> pairs;
+  std::vector<CycleConstraint> cycles;
+  // Optional: for each variable, a clique id -- variables sharing an id must
+  // conflict pairwise. Supplied by the planner (one clique per graph node);
+  // left empty, the solver derives cliques from the pair list.
+  std::vector<int> clique_hint;
+};
+
+struct FusionPlan {
+  std::vector<int> selected;
+  double total_score = 0.0;
+};
+
+std::vector<PairConstraint> build_conflicts(const std::vector<FusionPattern>& patterns);
+FusionPlan solve(const IlpInstance& inst);
+FusionPlan solve_with_cycle_elimination(const Graph& g, const std::vector<FusionPattern>& patterns,
+                                        const std::vector<double>& scores);
+
+// Statistics of the last solve on this thread (search nodes, rounds).
+struct SolveStats {
+  long long nodes = 0;
+  int queries = 0;
+  int rounds = 0;
+};
+const SolveStats& last_solve_stats();
+
+}  // namespace stitch
