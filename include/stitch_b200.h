@@ -78,6 +78,11 @@ STITCH_API int stitch_executor_run_host(stitch_executor* ex, const void* const* 
 STITCH_API int stitch_executor_profile(stitch_executor* ex, const void* const* inputs, void* const* outputs, void* stream,
                             int iters, char** json);
 
+/* Generated CUDA source of every kernel, {"<kernel name>": "<source>"}
+ * (the inspectable counterpart of the reference's emitted <fused_op>.cu
+ * files, pipeline.cpp:99 / stitch_main.cpp cmd_codegen). */
+STITCH_API char* stitch_executor_sources(const stitch_executor* ex);
+
 /* ---- misc ------------------------------------------------------------------ */
 STITCH_API const char* stitch_last_error(void);
 STITCH_API void stitch_free(char* p);

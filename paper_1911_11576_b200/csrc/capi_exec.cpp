@@ -1,0 +1,94 @@
+// C ABI, execution half (declared in include/stitch_b200.h).
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "exec/runtime.hpp"
+#include "capi_common.hpp"
+#include "stitch_b200.h"
+
+using namespace stitch;
+
+struct stitch_executor {
+  std::unique_ptr<exec::Executor> impl;
+};
+
+namespace {
+
+#define g_exec_error capi_last_error()
+
+char* dup(const std::string& s) {
+  char* p = static_cast<char*>(std::malloc(s.size() + 1));
+  std::memcpy(p, s.c_str(), s.size() + 1);
+  return p;
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const ParseError& e) {
+    g_exec_error = e.what();
+    return 1;
+  } catch (const ValidationError& e) {
+    g_exec_error = e.what();
+    return 1;
+  } catch (const std::exception& e) {
+    g_exec_error = e.what();
+    return 2;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int stitch_executor_create(const char* fused_graph_json, const char* options_json, stitch_executor** out) {
+  *out = nullptr;
+  return guarded([&] {
+    json::Value o = options_json && *options_json ? json::parse(options_json) : json::Value::object();
+    exec::ExecOptions opts;
+    if (o.has("device")) opts.device = static_cast<int>(o.at("device").as_int());
+    if (o.has("cache_dir")) opts.cache_dir = o.at("cache_dir").as_string();
+    if (o.has("use_graph")) opts.use_graph = o.at("use_graph").as_bool();
+    if (o.has("compile_only")) opts.compile_only = o.at("compile_only").as_bool();
+    if (o.has("smem_limit_bytes")) opts.codegen.max_smem = static_cast<int>(o.at("smem_limit_bytes").as_int());
+    if (o.has("allow_row")) opts.codegen.allow_row = o.at("allow_row").as_bool();
+    if (o.has("num_sms")) opts.codegen.num_sms = static_cast<int>(o.at("num_sms").as_int());
+    Graph g = parse_graph(fused_graph_json);
+    auto* ex = new stitch_executor;
+    ex->impl = std::make_unique<exec::Executor>(g, opts);
+    *out = ex;
+  });
+}
+
+void stitch_executor_destroy(stitch_executor* ex) { delete ex; }
+
+int stitch_executor_describe(const stitch_executor* ex, char** json_out) {
+  return guarded([&] { *json_out = dup(ex->impl->describe().dump()); });
+}
+
+int stitch_executor_run(stitch_executor* ex, const void* const* inputs, void* const* outputs, void* stream) {
+  return guarded([&] { ex->impl->run(inputs, outputs, stream); });
+}
+
+int stitch_executor_run_host(stitch_executor* ex, const void* const* host_inputs, void* const* host_outputs,
+                             void* stream) {
+  return guarded([&] { ex->impl->run_host(host_inputs, host_outputs, stream); });
+}
+
+int stitch_executor_profile(stitch_executor* ex, const void* const* inputs, void* const* outputs, void* stream,
+                            int iters, char** json_out) {
+  return guarded([&] { *json_out = dup(ex->impl->profile(inputs, outputs, stream, iters).dump()); });
+}
+
+// Generated source of every kernel (debugging / golden tests): {"name": src}.
+char* stitch_executor_sources(const stitch_executor* ex) {
+  json::Value o = json::Value::object();
+  for (const exec::KernelInst& k : ex->impl->kernels()) o.set(k.spec.name, exec::full_source(k.spec));
+  return dup(o.dump());
+}
+
+}  // extern "C"

@@ -6,13 +6,14 @@
 #include <string>
 
 #include "host/pipeline.hpp"
+#include "capi_common.hpp"
 #include "stitch_b200.h"
 
 using namespace stitch;
 
 namespace {
 
-thread_local std::string g_error;
+#define g_error capi_last_error()
 
 char* dup(const std::string& s) {
   char* p = static_cast<char*>(std::malloc(s.size() + 1));

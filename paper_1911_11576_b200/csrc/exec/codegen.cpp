@@ -1,0 +1,1404 @@
+// Stitched-kernel generator (see codegen.hpp for the scheme overview).
+//
+// Value semantics follow the reference emitter's per-op C expressions
+// (proj/src/emitter.cpp:793-829) and broadcast indexing (graph.cpp:146):
+// out[c] = in[c[map[0]], ..., c[map[r-1]]] with map the right-most greedy
+// subsequence match. Reductions: sum (reference) or max (extension).
+#include "codegen.hpp"
+
+#include <algorithm>
+#include <cstring>
+#include <functional>
+#include <numeric>
+#include <sstream>
+
+namespace stitch {
+namespace exec {
+
+namespace {
+
+std::string flit(double v) {
+  float f = static_cast<float>(v);
+  uint32_t bits;
+  std::memcpy(&bits, &f, 4);
+  char buf[64];
+  std::snprintf(buf, sizeof buf, "__int_as_float(0x%08x)", bits);
+  return buf;
+}
+
+int64_t prod(const std::vector<int64_t>& d, size_t from = 0, size_t to = std::string::npos) {
+  int64_t p = 1;
+  for (size_t i = from; i < std::min(to, d.size()); ++i) p *= d[i];
+  return p;
+}
+
+std::string join(const std::vector<std::string>& xs, const char* sep) {
+  std::string s;
+  for (size_t i = 0; i < xs.size(); ++i) s += (i ? sep : "") + xs[i];
+  return s;
+}
+
+// Row-major linear index of `coords` in `dims`, as a C expression.
+std::string linear(const std::vector<std::string>& coords, const std::vector<int64_t>& dims) {
+  if (coords.empty()) return "0";
+  std::string e = "(long long)(" + coords[0] + ")";
+  for (size_t i = 1; i < coords.size(); ++i) e = "(" + e + " * " + std::to_string(dims[i]) + "LL + (" + coords[i] + "))";
+  return e;
+}
+
+// Coordinates of linear index `lin` (a C expression) in `dims`.
+std::vector<std::string> decode(const std::string& lin, const std::vector<int64_t>& dims) {
+  std::vector<std::string> c(dims.size());
+  int64_t stride = 1;
+  for (size_t i = dims.size(); i-- > 0;) {
+    std::string e = stride == 1 ? "(" + lin + ")" : "((" + lin + ") / " + std::to_string(stride) + "LL)";
+    c[i] = i == 0 ? e : "(" + e + " % " + std::to_string(dims[i]) + "LL)";
+    stride *= dims[i];
+  }
+  return c;
+}
+
+enum class Cls { kNone, kRowed, kFree, kCross, kPost };
+
+struct Val {
+  std::string id;
+  const OpNode* node = nullptr;
+  bool external = false;
+  bool constant = false;
+  double cval = 0.0;
+  bool member = false;
+  bool output = false;
+  std::vector<int64_t> dims;
+  std::vector<int> operands;   // value indices
+  std::vector<int> consumers;  // member value indices (dups removed)
+};
+
+struct Layout {  // per-thread ownership of an inner tile of S elements
+  int64_t S = 1;
+  int vec = 1, iters = 1;
+  bool guard = false;
+  int elems() const { return vec * iters; }
+};
+
+struct Component {
+  std::vector<int> members;  // topo order
+  std::vector<int> outputs;
+  std::string scheme;        // row | flat | sectioned
+  int64_t weight = 1;
+  // ROW
+  int k = 0;
+  std::vector<int64_t> P;
+  int64_t R = 0;
+  int NT = 32;
+  bool cta = false;
+  std::vector<Cls> cls;
+  std::vector<char> staged;
+  std::vector<int64_t> smem_off;  // floats within the row-group slab
+  int64_t slab_floats = 0;
+  bool tma = false;
+  std::vector<int> cross, post, free_out;
+  int64_t max_grid = 1;
+};
+
+class Builder {
+ public:
+  Builder(const Graph& body, const std::string& name, const std::map<std::string, double>& constants,
+          const CodegenOptions& opts)
+      : body_(body), name_(name), consts_(constants), opts_(opts) {}
+
+  KernelSpec build();
+
+ private:
+  // ---- analysis ----
+  void collect();
+  std::vector<Component> components();
+  bool plan_row(Component& c);
+  bool all_elementwise(const Component& c) const;
+  Layout layout(int64_t S, int NT) const;
+  bool identity_broadcast(int in, int out, int k) const;
+
+  // ---- emission helpers ----
+  void ln(const std::string& s) { out_ << std::string(indent_ * 2, ' ') << s << "\n"; }
+  void open(const std::string& s) { ln(s + " {"); ++indent_; }
+  void close(const std::string& tail = "") { --indent_; ln("}" + tail); }
+  std::string fresh(const char* stem) { return std::string(stem) + std::to_string(tmp_++); }
+  std::string in_ptr(int v) const { return "in" + std::to_string(v); }
+  std::string out_ptr(int v) const { return "out" + std::to_string(v); }
+  std::string elem_expr(const OpNode& op, const std::vector<std::string>& a) const;
+  std::vector<std::string> map_broadcast(int in, int out, const std::vector<std::string>& coords) const;
+
+  // Inline expression machinery (FLAT / SECTIONED / FREE values).
+  std::string at(int v, const std::vector<std::string>& coords);
+  std::vector<std::map<std::string, std::string>> memo_;
+  std::map<int, std::string> materialized_;  // value -> buffer pointer expression (SECTIONED / post)
+  std::function<std::string(int, const std::vector<std::string>&)> row_hook_;
+
+  void emit_flat(const Component& c, const std::string& lo, const std::string& n);
+  void emit_row(Component& c, const std::string& lo, const std::string& n, const std::string& cta_rank);
+  void emit_row_finalize(std::vector<Component*>& comps);
+  void emit_sectioned(const std::vector<int>& members);
+
+  // ROW emission state
+  std::string row_access(const Component& c, int o, int v, const std::string& it, const std::string& u,
+                         const Layout& L);
+  std::map<int, std::string> reg_;  // value -> register array name (per row body)
+  std::map<int, std::string> scalar_;
+
+  const Graph& body_;
+  std::string name_;
+  const std::map<std::string, double>& consts_;
+  CodegenOptions opts_;
+
+  std::vector<Val> vals_;
+  std::map<std::string, int> idx_;
+  std::vector<int> topo_members_;
+  std::vector<int> outputs_;
+  std::vector<int> inputs_;  // pointer inputs
+
+  std::ostringstream out_;
+  int indent_ = 0;
+  int tmp_ = 0;
+  KernelSpec spec_;
+  int64_t ws_floats_ = 0;
+  bool uses_barrier_ = false;
+  std::map<int, int64_t> ws_off_;  // value -> workspace offset (floats)
+  std::map<int, std::string> cross_parts_;  // cross value -> nparts expression
+};
+
+// ---------------------------------------------------------------------------
+// analysis
+// ---------------------------------------------------------------------------
+
+void Builder::collect() {
+  const std::vector<std::string> topo = topological_sort(body_);
+  vals_.resize(body_.nodes.size());
+  for (size_t i = 0; i < body_.nodes.size(); ++i) {
+    const OpNode& n = body_.nodes[i];
+    Val& v = vals_[i];
+    v.id = n.id;
+    v.node = &n;
+    v.dims = n.shape.dims;
+    idx_[n.id] = static_cast<int>(i);
+    if (n.type == OpType::kParameter || n.type == OpType::kConstant) {
+      auto c = consts_.find(n.id);
+      if (c != consts_.end()) {
+        v.constant = true;
+        v.cval = c->second;
+      } else if (n.type == OpType::kConstant && n.value) {
+        v.constant = true;
+        v.cval = *n.value;
+      } else {
+        v.external = true;
+      }
+    } else if (is_fusible(n)) {
+      v.member = true;
+      if (n.shape.dtype != DType::f32())
+        throw GraphError("stitched executor: only f32 tensors are supported (" + n.id + ")");
+    }
+  }
+  for (size_t i = 0; i < body_.nodes.size(); ++i)
+    for (const std::string& o : body_.nodes[i].operands) vals_[i].operands.push_back(idx_.at(o));
+  for (const std::string& id : topo) {
+    int i = idx_.at(id);
+    if (!vals_[i].member) continue;
+    topo_members_.push_back(i);
+    for (int o : vals_[i].operands)
+      if (std::find(vals_[o].consumers.begin(), vals_[o].consumers.end(), i) == vals_[o].consumers.end())
+        vals_[o].consumers.push_back(i);
+  }
+  for (const OpNode& n : body_.nodes)
+    if (n.type == OpType::kTuple)
+      for (const std::string& o : n.operands) {
+        int i = idx_.at(o);
+        if (!vals_[i].member) throw GraphError("stitched executor: fused output " + o + " is not computed in the group");
+        if (!vals_[i].output) outputs_.push_back(i);
+        vals_[i].output = true;
+      }
+  if (outputs_.empty()) throw GraphError("stitched executor: fused body has no outputs");
+  for (int i = 0; i < static_cast<int>(vals_.size()); ++i)
+    if (vals_[i].external) {
+      bool used = !vals_[i].consumers.empty();
+      if (used) inputs_.push_back(i);
+      if (vals_[i].node->shape.dtype != DType::f32())
+        throw GraphError("stitched executor: only f32 tensors are supported (" + vals_[i].id + ")");
+    }
+}
+
+std::vector<Component> Builder::components() {
+  std::vector<int> parent(vals_.size());
+  std::iota(parent.begin(), parent.end(), 0);
+  std::function<int(int)> find = [&](int x) { return parent[x] == x ? x : parent[x] = find(parent[x]); };
+  for (int m : topo_members_)
+    for (int o : vals_[m].operands)
+      if (vals_[o].member) parent[find(m)] = find(o);
+  std::map<int, int> comp_of_root;
+  std::vector<Component> comps;
+  for (int m : topo_members_) {
+    int r = find(m);
+    auto it = comp_of_root.find(r);
+    if (it == comp_of_root.end()) {
+      it = comp_of_root.emplace(r, static_cast<int>(comps.size())).first;
+      comps.emplace_back();
+    }
+    comps[it->second].members.push_back(m);
+    if (vals_[m].output) comps[it->second].outputs.push_back(m);
+  }
+  for (Component& c : comps) {
+    int64_t w = 0;
+    std::set<int> ins;
+    for (int m : c.members)
+      for (int o : vals_[m].operands)
+        if (vals_[o].external) ins.insert(o);
+    for (int i : ins) w += vals_[i].node->shape.byte_count();
+    for (int o : c.outputs) w += vals_[o].node->shape.byte_count();
+    c.weight = std::max<int64_t>(w, 1);
+  }
+  return comps;
+}
+
+bool Builder::all_elementwise(const Component& c) const {
+  for (int m : c.members)
+    if (vals_[m].node->type != OpType::kElementwise) return false;
+  return true;
+}
+
+Layout Builder::layout(int64_t S, int NT) const {
+  Layout L;
+  L.S = S;
+  L.vec = S % 4 == 0 ? 4 : S % 2 == 0 ? 2 : 1;
+  if (S < NT * L.vec && S % NT == 0) L.vec = static_cast<int>(S / NT);  // spread small tiles over the group
+  if (L.vec < 1) L.vec = 1;
+  const int64_t per = static_cast<int64_t>(NT) * L.vec;
+  L.iters = static_cast<int>((S + per - 1) / per);
+  L.guard = S % per != 0;
+  return L;
+}
+
+std::vector<std::string> Builder::map_broadcast(int in, int out, const std::vector<std::string>& coords) const {
+  const Shape& is = vals_[in].node->shape;
+  const Shape& os = vals_[out].node->shape;
+  std::vector<int> m = broadcast_dim_map(is, os);
+  std::vector<std::string> c;
+  for (int d : m) c.push_back(coords[d]);
+  return c;
+}
+
+bool Builder::identity_broadcast(int in, int out, int k) const {
+  // Broadcast whose input, seen from the row tile, is indexed exactly like
+  // the output tile (same inner dims, inner map is the identity).
+  const auto& id = vals_[in].dims;
+  const auto& od = vals_[out].dims;
+  std::vector<int> m = broadcast_dim_map(vals_[in].node->shape, vals_[out].node->shape);
+  if (id.size() < static_cast<size_t>(k)) return false;
+  if (std::vector<int64_t>(id.begin() + k, id.end()) != std::vector<int64_t>(od.begin() + k, od.end())) return false;
+  for (size_t i = 0; i < m.size(); ++i)
+    if (m[i] != static_cast<int>(i)) return false;
+  return true;
+}
+
+bool Builder::plan_row(Component& c) {
+  if (!opts_.allow_row) return false;
+  // Anchor: the largest tensor the component touches.
+  int anchor = -1;
+  auto better = [&](int a) {
+    if (anchor < 0) return true;
+    int64_t ea = prod(vals_[a].dims), eb = prod(vals_[anchor].dims);
+    return ea > eb || (ea == eb && vals_[a].dims.size() > vals_[anchor].dims.size());
+  };
+  for (int m : c.members) {
+    if (better(m)) anchor = m;
+    for (int o : vals_[m].operands)
+      if (!vals_[o].constant && better(o)) anchor = o;
+  }
+  const std::vector<int64_t>& A = vals_[anchor].dims;
+  if (A.size() < 2) return false;
+
+  const int N = static_cast<int>(vals_.size());
+  int chosen_k = -1;
+  std::vector<Cls> best_cls;
+  for (int k = static_cast<int>(A.size()) - 1; k >= 1; --k) {
+    std::vector<int64_t> P(A.begin(), A.begin() + k);
+    auto rowed = [&](int v) {
+      const auto& d = vals_[v].dims;
+      return d.size() >= static_cast<size_t>(k) && std::equal(P.begin(), P.end(), d.begin());
+    };
+    std::vector<Cls> cls(N, Cls::kNone);
+    bool ok = true;
+    for (int v = 0; v < N; ++v)
+      if (vals_[v].external || vals_[v].constant) cls[v] = rowed(v) ? Cls::kRowed : Cls::kFree;
+    for (int m : c.members) {
+      const OpNode& op = *vals_[m].node;
+      const auto& ops = vals_[m].operands;
+      auto is_post_src = [&](int o) { return cls[o] == Cls::kCross || cls[o] == Cls::kPost; };
+      bool any_post = std::any_of(ops.begin(), ops.end(), is_post_src);
+      if (op.type == OpType::kElementwise) {
+        if (any_post) {
+          for (int o : ops)
+            if (cls[o] == Cls::kRowed) ok = false;
+          cls[m] = Cls::kPost;
+          continue;
+        }
+        if (op.elem_name == "broadcast") {
+          int in = ops[0];
+          if (rowed(m)) {
+            if (cls[in] == Cls::kRowed) {
+              std::vector<int> mp = broadcast_dim_map(vals_[in].node->shape, op.shape);
+              for (int i = 0; i < k; ++i) ok = ok && mp[i] == i;
+            } else {
+              std::vector<int> mp = broadcast_dim_map(vals_[in].node->shape, op.shape);
+              for (int d : mp) ok = ok && d >= k;
+            }
+            cls[m] = Cls::kRowed;
+          } else {
+            if (cls[in] == Cls::kRowed) ok = false;
+            cls[m] = Cls::kFree;
+          }
+        } else {
+          Cls want = rowed(m) ? Cls::kRowed : Cls::kFree;
+          for (int o : ops)
+            if (!vals_[o].constant && cls[o] != want) ok = false;
+          cls[m] = want;
+        }
+      } else if (op.type == OpType::kReduce) {
+        int in = ops[0];
+        if (cls[in] != Cls::kRowed) {
+          ok = false;
+          break;
+        }
+        int nrow = 0;
+        for (int d : op.reduce_dims) nrow += d < k;
+        const int rank_in = static_cast<int>(vals_[in].dims.size());
+        if (nrow == 0) {
+          cls[m] = Cls::kRowed;
+        } else if (nrow == k && (static_cast<int>(op.reduce_dims.size()) == k ||
+                                 static_cast<int>(op.reduce_dims.size()) == rank_in)) {
+          cls[m] = Cls::kCross;
+        } else {
+          ok = false;
+        }
+      } else if (op.type == OpType::kBatchedDot) {
+        int r = static_cast<int>(op.shape.dims.size());
+        ok = ok && k <= r - 2 && cls[ops[0]] == Cls::kRowed && cls[ops[1]] == Cls::kRowed;
+        cls[m] = Cls::kRowed;
+      } else if (op.type == OpType::kDot) {
+        auto cd = effective_contract_dims(body_, op);
+        ok = ok && cls[ops[0]] == Cls::kRowed && cd[0] >= k && cls[ops[1]] == Cls::kFree &&
+             vals_[ops[1]].external;
+        cls[m] = Cls::kRowed;
+      } else {
+        ok = false;
+      }
+      if (!ok) break;
+      // A rowed op may not consume post-phase values.
+      if (cls[m] == Cls::kRowed && any_post) ok = false;
+      if (!ok) break;
+    }
+    if (!ok) continue;
+    // Free members must be pure elementwise over free / constant inputs.
+    for (int m : c.members)
+      if (cls[m] == Cls::kFree && vals_[m].node->type != OpType::kElementwise) ok = false;
+    if (!ok) continue;
+    const int64_t inner = prod(A, k);
+    if (chosen_k < 0) {
+      chosen_k = k;
+      best_cls = cls;
+    }
+    if (inner >= 128) {
+      chosen_k = k;
+      best_cls = cls;
+      break;
+    }
+  }
+  if (chosen_k < 0) return false;
+  const int k = chosen_k;
+  c.k = k;
+  c.P.assign(A.begin(), A.begin() + k);
+  c.R = prod(c.P);
+  c.cls = best_cls;
+  c.staged.assign(N, 0);
+
+  bool has_dot = false;
+  int64_t max_inner = 1;
+  for (int m : c.members) {
+    const OpNode& op = *vals_[m].node;
+    if (c.cls[m] == Cls::kRowed) max_inner = std::max(max_inner, prod(vals_[m].dims, k));
+    for (int o : vals_[m].operands)
+      if (c.cls[o] == Cls::kRowed && !vals_[o].constant) max_inner = std::max(max_inner, prod(vals_[o].dims, k));
+    if (op.type == OpType::kBatchedDot || op.type == OpType::kDot) {
+      has_dot = true;
+      c.staged[vals_[m].operands[0]] = 1;
+      if (op.type == OpType::kBatchedDot) c.staged[vals_[m].operands[1]] = 1;
+    }
+    if (op.type == OpType::kReduce && c.cls[m] == Cls::kRowed) {
+      int in = vals_[m].operands[0];
+      int n_inner = static_cast<int>(vals_[in].dims.size()) - k;
+      if (static_cast<int>(op.reduce_dims.size()) != n_inner) c.staged[in] = 1;  // partial in-row reduce
+    }
+    if (op.type == OpType::kElementwise && op.elem_name == "broadcast" && c.cls[m] == Cls::kRowed) {
+      int in = vals_[m].operands[0];
+      if (c.cls[in] == Cls::kRowed && prod(vals_[in].dims, k) > 1 && !identity_broadcast(in, m, k) &&
+          !vals_[in].external)
+        c.staged[in] = 1;
+    }
+    if (c.cls[m] == Cls::kCross) c.cross.push_back(m);
+    if (c.cls[m] == Cls::kPost) c.post.push_back(m);
+    if (c.cls[m] == Cls::kFree && vals_[m].output) c.free_out.push_back(m);
+  }
+  bool any_staged = std::any_of(c.staged.begin(), c.staged.end(), [](char s) { return s != 0; });
+  c.cta = has_dot || any_staged || max_inner > 1024;
+  if (c.cta) {
+    int nt = 256;
+    if (max_inner > 4096) nt = 512;
+    if (max_inner > 8192) nt = 1024;
+    c.NT = nt;
+  } else {
+    c.NT = 32;
+  }
+  if (max_inner > static_cast<int64_t>(c.NT) * 64) return false;  // too large for registers
+  // shared-memory slab per row group
+  int64_t off = 0;
+  for (int v = 0; v < N; ++v)
+    if (c.staged[v]) {
+      c.smem_off.resize(N, -1);
+      c.smem_off[v] = off;
+      off += (prod(vals_[v].dims, k) + 3) / 4 * 4;
+    }
+  c.smem_off.resize(N, -1);
+  c.slab_floats = off;
+  if (c.cta) {
+    bool tma_ok = true;
+    for (int v = 0; v < N; ++v)
+      if (c.staged[v] && vals_[v].external) tma_ok = tma_ok && prod(vals_[v].dims, k) % 4 == 0;
+    c.tma = tma_ok && std::any_of(inputs_.begin(), inputs_.end(), [&](int v) { return c.staged[v] != 0; });
+  }
+  const int64_t slab_bytes = (c.slab_floats + 32) * 4;
+  if (c.cta ? slab_bytes > opts_.max_smem : slab_bytes * 8 > opts_.max_smem) return false;
+  c.scheme = "row";
+  c.max_grid = c.cta ? c.R : (c.R + 7) / 8;
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// expressions
+// ---------------------------------------------------------------------------
+
+std::string Builder::elem_expr(const OpNode& op, const std::vector<std::string>& a) const {
+  const std::string& f = op.elem_name;
+  if (f == "add") return "(" + a[0] + " + " + a[1] + ")";
+  if (f == "subtract") return "(" + a[0] + " - " + a[1] + ")";
+  if (f == "multiply") return "(" + a[0] + " * " + a[1] + ")";
+  if (f == "divide") return "(" + a[0] + " / " + a[1] + ")";
+  if (f == "maximum") return "fmaxf(" + a[0] + ", " + a[1] + ")";
+  if (f == "minimum") return "fminf(" + a[0] + ", " + a[1] + ")";
+  if (f == "log") return "logf(" + a[0] + ")";
+  if (f == "exp") return "expf(" + a[0] + ")";
+  if (f == "negate") return "(-" + a[0] + ")";
+  if (f == "rsqrt") return "rsqrtf(" + a[0] + ")";
+  if (f == "compare") return "stitch_dev::op_compare(" + a[0] + ", " + a[1] + ")";
+  if (f == "select") return "stitch_dev::op_select(" + a[0] + ", " + a[1] + ", " + a[2] + ")";
+  if (f == "broadcast") return a[0];
+  throw GraphError("stitched executor: unknown elementwise op " + f);
+}
+
+std::string Builder::at(int v, const std::vector<std::string>& coords) {
+  const Val& x = vals_[v];
+  if (x.constant) return flit(x.cval);
+  const std::string key = std::to_string(v) + "@" + join(coords, ",");
+  for (auto it = memo_.rbegin(); it != memo_.rend(); ++it) {
+    auto f = it->find(key);
+    if (f != it->end()) return f->second;
+  }
+  std::string expr;
+  auto m = materialized_.find(v);
+  if (row_hook_) {
+    std::string h = row_hook_(v, coords);
+    if (!h.empty()) return h;
+  }
+  if (m != materialized_.end()) {
+    expr = "__ldcg(" + m->second + " + " + linear(coords, x.dims) + ")";
+  } else if (x.external) {
+    expr = "__ldg(" + in_ptr(v) + " + " + linear(coords, x.dims) + ")";
+  } else if (x.member && x.node->type == OpType::kElementwise) {
+    std::vector<std::string> args;
+    if (x.node->elem_name == "broadcast") {
+      args.push_back(at(x.operands[0], map_broadcast(x.operands[0], v, coords)));
+    } else {
+      for (int o : x.operands) args.push_back(at(o, coords));
+    }
+    expr = elem_expr(*x.node, args);
+  } else {
+    throw InternalError("stitched executor: value " + x.id + " needed inline but not materialised");
+  }
+  std::string t = fresh("t");
+  ln("const float " + t + " = " + expr + ";  // " + x.id);
+  memo_.back()[key] = t;
+  return t;
+}
+
+// ---------------------------------------------------------------------------
+// FLAT: vectorised grid-stride loops, one per output shape
+// ---------------------------------------------------------------------------
+
+void Builder::emit_flat(const Component& c, const std::string& lo, const std::string& n) {
+  std::map<std::vector<int64_t>, std::vector<int>> by_shape;
+  for (int o : c.outputs) by_shape[vals_[o].dims].push_back(o);
+  for (auto& [dims, outs] : by_shape) {
+    const int64_t total = prod(dims);
+    const int64_t last = dims.empty() ? 1 : dims.back();
+    const int vec = (last % 4 == 0) ? 4 : 1;
+    const int64_t chunks = total / vec;
+    open("");
+    ln("// flat section over [" + [&] {
+      std::string s;
+      for (size_t i = 0; i < dims.size(); ++i) s += (i ? "," : "") + std::to_string(dims[i]);
+      return s;
+    }() + "]");
+    open("for (long long e = (long long)(blockIdx.x - " + lo + ") * blockDim.x + threadIdx.x; e < " +
+         std::to_string(chunks) + "LL; e += (long long)(" + n + ") * blockDim.x)");
+    memo_.emplace_back();
+    ln("const long long base = e * " + std::to_string(vec) + "LL;");
+    std::vector<std::string> bc = decode("base", dims);
+    std::map<int, std::vector<std::string>> results;
+    // Identity loads of same-shaped inputs as one 128-bit load.
+    if (vec == 4) {
+      std::set<int> ins, seen;
+      std::function<void(int)> walk = [&](int v) {
+        if (!seen.insert(v).second) return;
+        if (vals_[v].external && vals_[v].dims == dims) ins.insert(v);
+        if (vals_[v].member && !(vals_[v].node->elem_name == "broadcast"))
+          for (int o : vals_[v].operands) walk(o);
+      };
+      for (int o : outs) walk(o);
+      for (int v : ins) {
+        std::string t = fresh("q");
+        ln("const float4 " + t + " = stitch_dev::ld4_stream(" + in_ptr(v) + " + base);");
+        const char* lane[4] = {".x", ".y", ".z", ".w"};
+        for (int u = 0; u < 4; ++u) {
+          std::vector<std::string> cu = bc;
+          if (!cu.empty() && u) cu.back() = "(" + bc.back() + " + " + std::to_string(u) + ")";
+          memo_.back()[std::to_string(v) + "@" + join(cu, ",")] = t + lane[u];
+        }
+      }
+    }
+    for (int u = 0; u < vec; ++u) {
+      std::vector<std::string> cu = bc;
+      if (!cu.empty() && u) cu.back() = "(" + bc.back() + " + " + std::to_string(u) + ")";
+      for (int o : outs) results[o].push_back(at(o, cu));
+    }
+    for (int o : outs) {
+      if (vec == 4)
+        ln("stitch_dev::st4(" + out_ptr(o) + " + base, " + join(results[o], ", ") + ");");
+      else
+        ln(out_ptr(o) + "[base] = " + results[o][0] + ";");
+    }
+    memo_.pop_back();
+    close();
+    close();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// ROW
+// ---------------------------------------------------------------------------
+
+// Expression for operand `o` of rowed value `v` at v's owned element (it, u).
+std::string Builder::row_access(const Component& c, int o, int v, const std::string& it, const std::string& u,
+                                const Layout& L) {
+  const Val& x = vals_[o];
+  if (x.constant) return flit(x.cval);
+  const int k = c.k;
+  const std::string e = "(" + it + ") * " + std::to_string(L.vec) + " + (" + u + ")";
+  const std::string lin = "((" + it + ") * " + std::to_string(c.NT) + " + t) * " + std::to_string(L.vec) + " + (" + u + ")";
+  if (c.cls[o] == Cls::kRowed) {
+    const int64_t So = prod(x.dims, k);
+    if (So == 1) {
+      auto s = scalar_.find(o);
+      if (s != scalar_.end()) return s->second;
+      if (x.external) return "__ldg(" + in_ptr(o) + " + row)";
+    }
+    const bool ident = (vals_[v].node->type == OpType::kElementwise &&
+                        (vals_[v].node->elem_name != "broadcast" || identity_broadcast(o, v, k)));
+    if (ident) {
+      auto r = reg_.find(o);
+      if (r != reg_.end()) return r->second + "[" + e + "]";
+      if (c.staged[o]) return "sm" + std::to_string(o) + "[" + lin + "]";
+      if (x.external) return "__ldg(" + in_ptr(o) + " + row * " + std::to_string(So) + "LL + " + lin + ")";
+    }
+    // Gather through the broadcast map within the row.
+    std::vector<int64_t> vin(vals_[v].dims.begin() + k, vals_[v].dims.end());
+    std::vector<std::string> vc = decode(lin, vin);
+    std::vector<std::string> full;
+    for (int i = 0; i < k; ++i) full.push_back("0");
+    full.insert(full.end(), vc.begin(), vc.end());
+    std::vector<std::string> oc = map_broadcast(o, v, full);
+    std::vector<std::string> oin(oc.begin() + k, oc.end());
+    std::vector<int64_t> odims(x.dims.begin() + k, x.dims.end());
+    const std::string olin = linear(oin, odims);
+    if (c.staged[o]) return "sm" + std::to_string(o) + "[" + olin + "]";
+    if (x.external) return "__ldg(" + in_ptr(o) + " + row * " + std::to_string(So) + "LL + " + olin + ")";
+    throw InternalError("stitched executor: rowed value " + x.id + " gathered without staging");
+  }
+  // free operand: inline expression at the mapped coordinates
+  std::vector<int64_t> vin(vals_[v].dims.begin() + k, vals_[v].dims.end());
+  std::vector<std::string> vc = decode(lin, vin);
+  std::vector<std::string> full;
+  for (int i = 0; i < k; ++i) full.push_back("0");
+  full.insert(full.end(), vc.begin(), vc.end());
+  std::vector<std::string> oc = (vals_[v].node->elem_name == "broadcast") ? map_broadcast(o, v, full) : full;
+  // Same-shape free input read at the identity element: vector-friendly index.
+  if (x.external && x.dims == vin && vals_[v].node->elem_name != "broadcast") return "__ldg(" + in_ptr(o) + " + " + lin + ")";
+  if (x.external && vals_[v].node->elem_name == "broadcast" && x.dims == vin) {
+    std::vector<int> mp = broadcast_dim_map(x.node->shape, vals_[v].node->shape);
+    bool id = true;
+    for (size_t i = 0; i < mp.size(); ++i) id = id && mp[i] == static_cast<int>(i) + k;
+    if (id) return "__ldg(" + in_ptr(o) + " + " + lin + ")";
+  }
+  return at(o, oc);
+}
+
+void Builder::emit_row(Component& c, const std::string& lo, const std::string& n, const std::string& cta_rank) {
+  const int k = c.k;
+  const int NT = c.NT;
+  (void)cta_rank;
+  open("");
+  ln("// row scheme: k=" + std::to_string(k) + " rows=" + std::to_string(c.R) + " threads/row=" + std::to_string(NT));
+  if (c.cta) {
+    ln("const int t = threadIdx.x;");
+    ln("float* slab = smem;");
+    ln("const long long g0 = blockIdx.x - " + lo + ", gstride = " + n + ";");
+  } else {
+    ln("const int t = threadIdx.x & 31;");
+    ln("const int wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;");
+    ln("float* slab = smem + wib * " + std::to_string(c.slab_floats + 32) + ";");
+    ln("const long long g0 = (long long)(blockIdx.x - " + lo + ") * wpb + wib, gstride = (long long)(" + n + ") * wpb;");
+  }
+  ln("float* red = slab + " + std::to_string(c.slab_floats) + ";");
+  ln("(void)red;");
+  for (int v = 0; v < static_cast<int>(vals_.size()); ++v)
+    if (c.staged[v]) ln("float* sm" + std::to_string(v) + " = slab + " + std::to_string(c.smem_off[v]) + ";  // " + vals_[v].id);
+
+  // Free outputs (not depending on rows): grid-stride over their elements.
+  for (int f : c.free_out) {
+    open("for (long long i = (long long)(blockIdx.x - " + lo + ") * blockDim.x + threadIdx.x; i < " +
+         std::to_string(prod(vals_[f].dims)) + "LL; i += (long long)(" + n + ") * blockDim.x)");
+    memo_.emplace_back();
+    ln(out_ptr(f) + "[i] = " + at(f, decode("i", vals_[f].dims)) + ";");
+    memo_.pop_back();
+    close();
+  }
+
+  // Cross-row partial accumulators.
+  std::map<int, Layout> cross_layout;
+  for (int x : c.cross) {
+    const OpNode& op = *vals_[x].node;
+    int in = vals_[x].operands[0];
+    Layout L = layout(prod(vals_[in].dims, k), NT);
+    cross_layout[x] = L;
+    bool scalar = static_cast<int>(op.reduce_dims.size()) == static_cast<int>(vals_[in].dims.size());
+    const std::string Op = op.elem_name == "max" ? "stitch_dev::MaxOp" : "stitch_dev::SumOp";
+    if (scalar)
+      ln("float p" + std::to_string(x) + " = " + Op + "::init();  // " + vals_[x].id);
+    else {
+      ln("float p" + std::to_string(x) + "[" + std::to_string(L.elems()) + "];  // " + vals_[x].id);
+      ln("#pragma unroll");
+      ln("for (int e = 0; e < " + std::to_string(L.elems()) + "; ++e) p" + std::to_string(x) + "[e] = " + Op + "::init();");
+    }
+  }
+
+  if (c.tma) {
+    ln("stitch_dev::u64* bar = reinterpret_cast<stitch_dev::u64*>(smem + " + std::to_string(c.slab_floats + 32) + ");");
+    ln("if (t == 0) stitch_dev::mbar_init(bar, 1);");
+    ln("__syncthreads();");
+    ln("unsigned phase = 0;");
+  }
+  open("for (long long row = g0; row < " + std::to_string(c.R) + "LL; row += gstride)");
+  reg_.clear();
+  scalar_.clear();
+  memo_.emplace_back();
+  const std::string sync = c.cta ? "__syncthreads();" : "__syncwarp();";
+
+  // Stage external operand tiles (TMA bulk copies in CTA mode).
+  bool any_ext_staged = false;
+  for (int v : inputs_)
+    if (c.staged[v]) any_ext_staged = true;
+  if (any_ext_staged) {
+    if (c.tma) {
+      int64_t bytes = 0;
+      for (int v : inputs_)
+        if (c.staged[v]) bytes += prod(vals_[v].dims, k) * 4;
+      open("if (t == 0)");
+      ln("stitch_dev::mbar_expect_tx(bar, " + std::to_string(bytes) + "u);");
+      for (int v : inputs_)
+        if (c.staged[v]) {
+          const int64_t S = prod(vals_[v].dims, k);
+          ln("stitch_dev::bulk_g2s(sm" + std::to_string(v) + ", " + in_ptr(v) + " + row * " + std::to_string(S) +
+             "LL, " + std::to_string(S * 4) + "u, bar);");
+        }
+      close();
+      ln("stitch_dev::mbar_wait(bar, phase);");
+      ln("phase ^= 1u;");
+    } else {
+      for (int v : inputs_)
+        if (c.staged[v]) {
+          const int64_t S = prod(vals_[v].dims, k);
+          ln("for (int i = t; i < " + std::to_string(S) + "; i += " + std::to_string(NT) + ") sm" + std::to_string(v) +
+             "[i] = __ldg(" + in_ptr(v) + " + row * " + std::to_string(S) + "LL + i);");
+        }
+      ln(sync);
+    }
+  }
+
+  // Register loads of rowed inputs read at identity by elementwise ops.
+  for (int v : inputs_) {
+    if (c.cls[v] != Cls::kRowed || c.staged[v]) continue;
+    const int64_t S = prod(vals_[v].dims, k);
+    if (S == 1) {
+      std::string s = fresh("s");
+      ln("const float " + s + " = __ldg(" + in_ptr(v) + " + row);  // " + vals_[v].id);
+      scalar_[v] = s;
+      continue;
+    }
+    bool ident_use = false;
+    for (int m : vals_[v].consumers) {
+      if (std::find(c.members.begin(), c.members.end(), m) == c.members.end()) continue;
+      const OpNode& op = *vals_[m].node;
+      if (op.type == OpType::kReduce) ident_use = true;
+      if (op.type == OpType::kElementwise && (op.elem_name != "broadcast" || identity_broadcast(v, m, k)))
+        ident_use = true;
+    }
+    if (!ident_use) continue;
+    Layout L = layout(S, NT);
+    std::string r = "r" + std::to_string(v);
+    ln("float " + r + "[" + std::to_string(L.elems()) + "];  // " + vals_[v].id);
+    ln("#pragma unroll");
+    open("for (int it = 0; it < " + std::to_string(L.iters) + "; ++it)");
+    ln("const int lin = (it * " + std::to_string(NT) + " + t) * " + std::to_string(L.vec) + ";");
+    if (L.guard) open("if (lin < " + std::to_string(S) + ")");
+    const std::string src = in_ptr(v) + " + row * " + std::to_string(S) + "LL + lin";
+    if (L.vec == 4) {
+      ln("const float4 q = stitch_dev::ld4_stream(" + src + ");");
+      ln(r + "[it * 4 + 0] = q.x; " + r + "[it * 4 + 1] = q.y; " + r + "[it * 4 + 2] = q.z; " + r + "[it * 4 + 3] = q.w;");
+    } else {
+      for (int u = 0; u < L.vec; ++u) ln(r + "[it * " + std::to_string(L.vec) + " + " + std::to_string(u) + "] = __ldg(" + src + " + " + std::to_string(u) + ");");
+    }
+    if (L.guard) {
+      close();
+      ln("else { for (int u = 0; u < " + std::to_string(L.vec) + "; ++u) " + r + "[it * " + std::to_string(L.vec) + " + u] = 0.0f; }");
+    }
+    close();
+    reg_[v] = r;
+  }
+
+  auto emit_elementwise_loop = [&](int m, const Layout& L, const std::function<std::string(const std::string&, const std::string&)>& body_fn) {
+    std::string r = "r" + std::to_string(m);
+    ln("float " + r + "[" + std::to_string(L.elems()) + "];  // " + vals_[m].id);
+    ln("#pragma unroll");
+    open("for (int it = 0; it < " + std::to_string(L.iters) + "; ++it)");
+    ln("#pragma unroll");
+    open("for (int u = 0; u < " + std::to_string(L.vec) + "; ++u)");
+    memo_.emplace_back();
+    if (L.guard) {
+      ln("const int lin_g = (it * " + std::to_string(NT) + " + t) * " + std::to_string(L.vec) + " + u;");
+      open("if (lin_g < " + std::to_string(L.S) + ")");
+    }
+    ln(r + "[it * " + std::to_string(L.vec) + " + u] = " + body_fn("it", "u") + ";");
+    if (L.guard) {
+      close();
+      ln("else " + r + "[it * " + std::to_string(L.vec) + " + u] = 0.0f;");
+    }
+    memo_.pop_back();
+    close();
+    close();
+    reg_[m] = r;
+  };
+
+  for (int m : c.members) {
+    if (c.cls[m] != Cls::kRowed) continue;
+    const OpNode& op = *vals_[m].node;
+    const int64_t S = prod(vals_[m].dims, k);
+    const Layout L = layout(S, NT);
+    if (op.type == OpType::kElementwise) {
+      if (S == 1) {
+        // row scalar: every thread holds the value
+        std::vector<std::string> args;
+        for (int o : vals_[m].operands) {
+          if (vals_[o].constant) args.push_back(flit(vals_[o].cval));
+          else if (c.cls[o] == Cls::kRowed) {
+            auto s = scalar_.find(o);
+            args.push_back(s != scalar_.end() ? s->second : "__ldg(" + in_ptr(o) + " + row)");
+          } else {
+            std::vector<std::string> zero(vals_[o].dims.size(), "0");
+            args.push_back(at(o, zero));
+          }
+        }
+        std::string s = fresh("s");
+        ln("const float " + s + " = " + elem_expr(op, args) + ";  // " + vals_[m].id);
+        scalar_[m] = s;
+      } else {
+        emit_elementwise_loop(m, L, [&](const std::string& it, const std::string& u) {
+          std::vector<std::string> args;
+          for (int o : vals_[m].operands) args.push_back(row_access(c, o, m, it, u, L));
+          return elem_expr(op, args);
+        });
+      }
+    } else if (op.type == OpType::kReduce) {
+      const int in = vals_[m].operands[0];
+      const std::string Op = op.elem_name == "max" ? "stitch_dev::MaxOp" : "stitch_dev::SumOp";
+      const int64_t Sin = prod(vals_[in].dims, k);
+      const Layout Li = layout(Sin, NT);
+      if (S == 1) {
+        std::string acc = fresh("a");
+        ln("float " + acc + " = " + Op + "::init();");
+        ln("#pragma unroll");
+        open("for (int it = 0; it < " + std::to_string(Li.iters) + "; ++it)");
+        ln("#pragma unroll");
+        open("for (int u = 0; u < " + std::to_string(Li.vec) + "; ++u)");
+        if (Li.guard) open("if ((it * " + std::to_string(NT) + " + t) * " + std::to_string(Li.vec) + " + u < " + std::to_string(Sin) + ")");
+        std::string x;
+        auto r = reg_.find(in);
+        if (r != reg_.end()) x = r->second + "[it * " + std::to_string(Li.vec) + " + u]";
+        else if (c.staged[in]) x = "sm" + std::to_string(in) + "[(it * " + std::to_string(NT) + " + t) * " + std::to_string(Li.vec) + " + u]";
+        else throw InternalError("row reduce input not in registers: " + vals_[in].id);
+        ln(acc + " = " + Op + "::apply(" + acc + ", " + x + ");");
+        if (Li.guard) close();
+        close();
+        close();
+        std::string s = fresh("s");
+        ln("const float " + s + " = stitch_dev::row_allreduce<" + std::to_string(NT) + ", " + Op + ">(" + acc + ", red);  // " + vals_[m].id);
+        scalar_[m] = s;
+      } else {
+        // partial in-row reduce from the staged input tile
+        std::vector<int64_t> ind(vals_[in].dims.begin() + k, vals_[in].dims.end());
+        emit_elementwise_loop(m, L, [&](const std::string& it, const std::string& u) {
+          std::string lin = "((" + it + ") * " + std::to_string(NT) + " + t) * " + std::to_string(L.vec) + " + (" + u + ")";
+          std::vector<int64_t> od(vals_[m].dims.begin() + k, vals_[m].dims.end());
+          std::vector<std::string> oc = decode(lin, od);
+          std::string acc = fresh("a");
+          ln("float " + acc + " = " + Op + "::init();");
+          std::vector<std::string> ic;
+          size_t kept = 0;
+          int loops = 0;
+          for (size_t d = 0; d < ind.size(); ++d) {
+            int gd = static_cast<int>(d) + k;
+            if (std::find(op.reduce_dims.begin(), op.reduce_dims.end(), gd) != op.reduce_dims.end()) {
+              std::string lv = fresh("q");
+              open("for (int " + lv + " = 0; " + lv + " < " + std::to_string(ind[d]) + "; ++" + lv + ")");
+              ++loops;
+              ic.push_back(lv);
+            } else {
+              ic.push_back(oc[kept++]);
+            }
+          }
+          ln(acc + " = " + Op + "::apply(" + acc + ", sm" + std::to_string(in) + "[" + linear(ic, ind) + "]);");
+          for (int i = 0; i < loops; ++i) close();
+          return acc;
+        });
+      }
+    } else if (op.type == OpType::kBatchedDot || op.type == OpType::kDot) {
+      const int a = vals_[m].operands[0], b = vals_[m].operands[1];
+      auto cd = effective_contract_dims(body_, op);
+      const int64_t K = vals_[a].dims[cd[0]];
+      std::vector<int64_t> od(vals_[m].dims.begin() + k, vals_[m].dims.end());
+      std::vector<int64_t> ad(vals_[a].dims.begin() + k, vals_[a].dims.end());
+      std::vector<int64_t> bd = op.type == OpType::kBatchedDot
+                                    ? std::vector<int64_t>(vals_[b].dims.begin() + k, vals_[b].dims.end())
+                                    : vals_[b].dims;
+      const int64_t Nn = od.back();
+      const bool fast = op.type == OpType::kBatchedDot && L.vec == 4 && Nn % 4 == 0 && !L.guard;
+      std::string r = "r" + std::to_string(m);
+      ln("float " + r + "[" + std::to_string(L.elems()) + "];  // " + vals_[m].id + " (gemm stage)");
+      if (fast) {
+        // Output element chunk (.., m, n0..n0+3) per (it): A scalar x B float4.
+        const int rb = static_cast<int>(od.size());
+        ln("#pragma unroll");
+        open("for (int it = 0; it < " + std::to_string(L.iters) + "; ++it)");
+        ln("const int lin = (it * " + std::to_string(NT) + " + t) * 4;");
+        std::vector<std::string> oc = decode("lin", od);
+        ln("const int n0 = (int)" + oc[rb - 1] + ";");
+        ln("const int mm = (int)" + oc[rb - 2] + ";");
+        std::string bb = "0";
+        {
+          std::vector<int64_t> bdims(od.begin(), od.end() - 2);
+          std::vector<std::string> bcs(oc.begin(), oc.end() - 2);
+          bb = linear(bcs, bdims);
+        }
+        ln("const long long bb = " + bb + ";");
+        ln("float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;");
+        const int64_t M = od[rb - 2];
+        ln("const float* A = sm" + std::to_string(a) + " + bb * " + std::to_string(M * K) + "LL + (long long)mm * " + std::to_string(K) + ";");
+        ln("const float* B = sm" + std::to_string(b) + " + bb * " + std::to_string(K * Nn) + "LL + n0;");
+        ln("#pragma unroll 8");
+        open("for (int kk = 0; kk < " + std::to_string(K) + "; ++kk)");
+        ln("const float av = A[kk];");
+        ln("const float4 bv = *reinterpret_cast<const float4*>(B + kk * " + std::to_string(Nn) + ");");
+        ln("c0 = fmaf(av, bv.x, c0); c1 = fmaf(av, bv.y, c1); c2 = fmaf(av, bv.z, c2); c3 = fmaf(av, bv.w, c3);");
+        close();
+        ln(r + "[it * 4 + 0] = c0; " + r + "[it * 4 + 1] = c1; " + r + "[it * 4 + 2] = c2; " + r + "[it * 4 + 3] = c3;");
+        close();
+      } else {
+        ln("#pragma unroll");
+        open("for (int it = 0; it < " + std::to_string(L.iters) + "; ++it)");
+        ln("#pragma unroll");
+        open("for (int u = 0; u < " + std::to_string(L.vec) + "; ++u)");
+        ln("const int lin = (it * " + std::to_string(NT) + " + t) * " + std::to_string(L.vec) + " + u;");
+        ln("float acc = 0.f;");
+        if (L.guard) open("if (lin < " + std::to_string(L.S) + ")");
+        std::vector<std::string> oc = decode("lin", od);
+        std::vector<std::string> ac, bc;
+        if (op.type == OpType::kBatchedDot) {
+          const int rb = static_cast<int>(od.size());
+          for (int d = 0; d < rb - 2; ++d) {
+            ac.push_back(oc[d]);
+            bc.push_back(oc[d]);
+          }
+          ac.push_back(oc[rb - 2]);
+          ac.push_back("kk");
+          bc.push_back("kk");
+          bc.push_back(oc[rb - 1]);
+        } else {
+          int pos = 0;
+          for (int d = k; d < static_cast<int>(vals_[a].dims.size()); ++d) ac.push_back(d == cd[0] ? "kk" : oc[pos++]);
+          for (int d = 0; d < static_cast<int>(vals_[b].dims.size()); ++d) bc.push_back(d == cd[1] ? "kk" : oc[pos++]);
+        }
+        open("for (int kk = 0; kk < " + std::to_string(K) + "; ++kk)");
+        std::string bval = op.type == OpType::kBatchedDot ? "sm" + std::to_string(b) + "[" + linear(bc, bd) + "]"
+                                                            : "__ldg(" + in_ptr(b) + " + " + linear(bc, bd) + ")";
+        ln("acc = fmaf(sm" + std::to_string(a) + "[" + linear(ac, ad) + "], " + bval + ", acc);");
+        close();
+        if (L.guard) close();
+        ln(r + "[it * " + std::to_string(L.vec) + " + u] = acc;");
+        close();
+        close();
+      }
+      reg_[m] = r;
+      int64_t mnk = prod(vals_[m].dims) * K;
+      spec_.flops += 2 * mnk;
+    }
+    // Stage computed values that later ops gather from.
+    if (c.staged[m]) {
+      ln(sync);  // previous readers of this slab region are done
+      ln("#pragma unroll");
+      open("for (int it = 0; it < " + std::to_string(L.iters) + "; ++it)");
+      ln("#pragma unroll");
+      open("for (int u = 0; u < " + std::to_string(L.vec) + "; ++u)");
+      ln("const int lin = (it * " + std::to_string(NT) + " + t) * " + std::to_string(L.vec) + " + u;");
+      std::string val = S == 1 ? scalar_[m] : reg_[m] + "[it * " + std::to_string(L.vec) + " + u]";
+      ln((L.guard ? "if (lin < " + std::to_string(S) + ") " : std::string()) + "sm" + std::to_string(m) + "[lin] = " + val + ";");
+      close();
+      close();
+      ln(sync);
+    }
+  }
+
+  // Cross-row accumulation.
+  for (int x : c.cross) {
+    const OpNode& op = *vals_[x].node;
+    const int in = vals_[x].operands[0];
+    const Layout& L = cross_layout[x];
+    const std::string Op = op.elem_name == "max" ? "stitch_dev::MaxOp" : "stitch_dev::SumOp";
+    bool scalar = static_cast<int>(op.reduce_dims.size()) == static_cast<int>(vals_[in].dims.size());
+    std::string src;
+    auto r = reg_.find(in);
+    ln("#pragma unroll");
+    open("for (int it = 0; it < " + std::to_string(L.iters) + "; ++it)");
+    ln("#pragma unroll");
+    open("for (int u = 0; u < " + std::to_string(L.vec) + "; ++u)");
+    ln("const int lin = (it * " + std::to_string(NT) + " + t) * " + std::to_string(L.vec) + " + u;");
+    if (r != reg_.end()) src = r->second + "[it * " + std::to_string(L.vec) + " + u]";
+    else if (c.staged[in]) src = "sm" + std::to_string(in) + "[lin]";
+    else if (scalar_.count(in)) src = scalar_[in];
+    else throw InternalError("cross-row reduce input unavailable: " + vals_[in].id);
+    std::string tgt = scalar ? "p" + std::to_string(x) : "p" + std::to_string(x) + "[it * " + std::to_string(L.vec) + " + u]";
+    ln((L.guard ? "if (lin < " + std::to_string(L.S) + ") " : std::string()) + tgt + " = " + Op + "::apply(" + tgt + ", " + src + ");");
+    close();
+    close();
+  }
+
+  // Row outputs.
+  for (int o : c.outputs) {
+    if (c.cls[o] != Cls::kRowed) continue;
+    const int64_t S = prod(vals_[o].dims, k);
+    if (S == 1) {
+      ln("if (t == 0) " + out_ptr(o) + "[row] = " + scalar_[o] + ";");
+      continue;
+    }
+    const Layout L = layout(S, NT);
+    const std::string r = reg_[o];
+    ln("#pragma unroll");
+    open("for (int it = 0; it < " + std::to_string(L.iters) + "; ++it)");
+    ln("const int lin = (it * " + std::to_string(NT) + " + t) * " + std::to_string(L.vec) + ";");
+    if (L.guard) open("if (lin < " + std::to_string(S) + ")");
+    const std::string dst = out_ptr(o) + " + row * " + std::to_string(S) + "LL + lin";
+    if (L.vec == 4)
+      ln("stitch_dev::st4(" + dst + ", " + r + "[it * 4], " + r + "[it * 4 + 1], " + r + "[it * 4 + 2], " + r + "[it * 4 + 3]);");
+    else
+      for (int u = 0; u < L.vec; ++u) ln("(" + dst + ")[" + std::to_string(u) + "] = " + r + "[it * " + std::to_string(L.vec) + " + " + std::to_string(u) + "];");
+    if (L.guard) close();
+    close();
+  }
+  memo_.pop_back();
+  if (c.cta && (any_ext_staged || std::any_of(c.staged.begin(), c.staged.end(), [](char s) { return s; }))) ln("__syncthreads();");
+  close();  // row loop
+
+  // Write this CTA's cross-row partials: combine the CTA's row groups first.
+  for (int x : c.cross) {
+    const OpNode& op = *vals_[x].node;
+    const int in = vals_[x].operands[0];
+    const Layout& L = cross_layout[x];
+    const std::string Op = op.elem_name == "max" ? "stitch_dev::MaxOp" : "stitch_dev::SumOp";
+    bool scalar = static_cast<int>(op.reduce_dims.size()) == static_cast<int>(vals_[in].dims.size());
+    const int64_t So = scalar ? 1 : L.S;
+    const std::string parts = "(ws + " + std::to_string(ws_off_[x]) + "LL)";
+    const std::string rank = "(long long)(blockIdx.x - " + lo + ")";
+    if (scalar) {
+      if (c.cta) {
+        ln("{ const float v = stitch_dev::row_allreduce<" + std::to_string(NT) + ", " + Op + ">(p" + std::to_string(x) + ", red);");
+        ln("  if (threadIdx.x == 0) " + parts + "[" + rank + "] = v; }");
+      } else {
+        ln("{ float v = stitch_dev::warp_allreduce<" + Op + ">(p" + std::to_string(x) + ");");
+        ln("  __syncthreads(); if (t == 0) smem[wib] = v; __syncthreads();");
+        ln("  if (threadIdx.x == 0) { float a = " + Op + "::init(); for (int w = 0; w < wpb; ++w) a = " + Op + "::apply(a, smem[w]); " + parts + "[" + rank + "] = a; }");
+        ln("  __syncthreads(); }");
+      }
+    } else if (c.cta) {
+      ln("#pragma unroll");
+      open("for (int it = 0; it < " + std::to_string(L.iters) + "; ++it)");
+      ln("#pragma unroll");
+      open("for (int u = 0; u < " + std::to_string(L.vec) + "; ++u)");
+      ln("const int lin = (it * " + std::to_string(NT) + " + t) * " + std::to_string(L.vec) + " + u;");
+      ln((L.guard ? "if (lin < " + std::to_string(So) + ") " : std::string()) + parts + "[" + rank + " * " + std::to_string(So) + "LL + lin] = p" + std::to_string(x) + "[it * " + std::to_string(L.vec) + " + u];");
+      close();
+      close();
+    } else {
+      // warps -> shared partial rows -> fixed-order CTA sum
+      ln("__syncthreads();");
+      ln("#pragma unroll");
+      open("for (int it = 0; it < " + std::to_string(L.iters) + "; ++it)");
+      ln("#pragma unroll");
+      open("for (int u = 0; u < " + std::to_string(L.vec) + "; ++u)");
+      ln("const int lin = (it * 32 + t) * " + std::to_string(L.vec) + " + u;");
+      ln((L.guard ? "if (lin < " + std::to_string(So) + ") " : std::string()) + "smem[wib * " + std::to_string(So) + " + lin] = p" + std::to_string(x) + "[it * " + std::to_string(L.vec) + " + u];");
+      close();
+      close();
+      ln("__syncthreads();");
+      open("for (int i = threadIdx.x; i < " + std::to_string(So) + "; i += blockDim.x)");
+      ln("float a = " + Op + "::init();");
+      ln("for (int w = 0; w < wpb; ++w) a = " + Op + "::apply(a, smem[w * " + std::to_string(So) + " + i]);");
+      ln(parts + "[" + rank + " * " + std::to_string(So) + "LL + i] = a;");
+      close();
+      ln("__syncthreads();");
+    }
+  }
+  close();
+}
+
+void Builder::emit_row_finalize(std::vector<Component*>& comps) {
+  bool any = false;
+  for (Component* c : comps) any = any || !c->cross.empty();
+  if (!any) return;
+  uses_barrier_ = true;
+  ln("stitch_dev::grid_barrier(gsync);");
+  ln("// deterministic combine of the per-CTA partials");
+  for (Component* c : comps)
+    for (int x : c->cross) {
+      const OpNode& op = *vals_[x].node;
+      const int in = vals_[x].operands[0];
+      bool scalar = static_cast<int>(op.reduce_dims.size()) == static_cast<int>(vals_[in].dims.size());
+      const int64_t So = scalar ? 1 : prod(vals_[in].dims, c->k);
+      const std::string Op = op.elem_name == "max" ? "stitch_dev::MaxOp" : "stitch_dev::SumOp";
+      open("for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < " + std::to_string(So) + "LL; i += (long long)gridDim.x * blockDim.x)");
+      ln("const float v = stitch_dev::combine_parts<" + Op + ">(ws + " + std::to_string(ws_off_[x]) + "LL, " + cross_parts_[x] + ", " + std::to_string(So) + "LL, i);");
+      if (vals_[x].output) ln(out_ptr(x) + "[i] = v;");
+      if (materialized_.count(x) && !vals_[x].output) ln(materialized_[x] + "[i] = v;");
+      close();
+    }
+  bool any_post = false;
+  for (Component* c : comps) any_post = any_post || !c->post.empty();
+  if (!any_post) return;
+  ln("stitch_dev::grid_barrier(gsync);");
+  for (Component* c : comps)
+    for (int p : c->post) {
+      if (!vals_[p].output) continue;
+      open("for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < " + std::to_string(prod(vals_[p].dims)) + "LL; i += (long long)gridDim.x * blockDim.x)");
+      memo_.emplace_back();
+      ln(out_ptr(p) + "[i] = " + at(p, decode("i", vals_[p].dims)) + ";");
+      memo_.pop_back();
+      close();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// SECTIONED
+// ---------------------------------------------------------------------------
+
+void Builder::emit_sectioned(const std::vector<int>& members) {
+  std::vector<int> mat;
+  for (int m : members) {
+    const Val& v = vals_[m];
+    bool need = v.output || v.node->type != OpType::kElementwise;
+    for (int c : v.consumers)
+      need = need || vals_[c].node->type == OpType::kDot || vals_[c].node->type == OpType::kBatchedDot;
+    if (need) mat.push_back(m);
+  }
+  for (int m : mat)
+    if (!vals_[m].output) {
+      ws_off_[m] = ws_floats_;
+      ws_floats_ += (prod(vals_[m].dims) + 63) / 64 * 64;
+    }
+  for (size_t s = 0; s < mat.size(); ++s) {
+    const int m = mat[s];
+    const Val& v = vals_[m];
+    const OpNode& op = *v.node;
+    const std::string dst = v.output ? out_ptr(m) : "(ws + " + std::to_string(ws_off_[m]) + "LL)";
+    if (s > 0) {
+      uses_barrier_ = true;
+      ln("stitch_dev::grid_barrier(gsync);");
+    }
+    ln("// section: " + v.id);
+    open("for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < " + std::to_string(prod(v.dims)) + "LL; i += (long long)gridDim.x * blockDim.x)");
+    memo_.emplace_back();
+    std::vector<std::string> oc = decode("i", v.dims);
+    if (op.type == OpType::kElementwise) {
+      ln(dst + "[i] = " + at(m, oc) + ";");
+    } else if (op.type == OpType::kReduce) {
+      const int in = v.operands[0];
+      const auto& ind = vals_[in].dims;
+      const std::string Op = op.elem_name == "max" ? "stitch_dev::MaxOp" : "stitch_dev::SumOp";
+      ln("float acc = " + Op + "::init();");
+      std::vector<std::string> ic;
+      size_t kept = 0;
+      int loops = 0;
+      for (size_t d = 0; d < ind.size(); ++d) {
+        if (std::find(op.reduce_dims.begin(), op.reduce_dims.end(), static_cast<int>(d)) != op.reduce_dims.end()) {
+          std::string lv = fresh("q");
+          open("for (long long " + lv + " = 0; " + lv + " < " + std::to_string(ind[d]) + "LL; ++" + lv + ")");
+          memo_.emplace_back();
+          ++loops;
+          ic.push_back(lv);
+        } else {
+          ic.push_back(oc[kept++]);
+        }
+      }
+      ln("acc = " + Op + "::apply(acc, " + at(in, ic) + ");");
+      for (int l = 0; l < loops; ++l) {
+        memo_.pop_back();
+        close();
+      }
+      ln(dst + "[i] = acc;");
+    } else if (op.type == OpType::kDot || op.type == OpType::kBatchedDot) {
+      const int a = v.operands[0], b = v.operands[1];
+      auto cd = effective_contract_dims(body_, op);
+      const int64_t K = vals_[a].dims[cd[0]];
+      std::vector<std::string> ac, bc;
+      if (op.type == OpType::kBatchedDot) {
+        const int r = static_cast<int>(v.dims.size());
+        for (int d = 0; d < r - 2; ++d) {
+          ac.push_back(oc[d]);
+          bc.push_back(oc[d]);
+        }
+        ac.push_back(oc[r - 2]);
+        ac.push_back("kk");
+        bc.push_back("kk");
+        bc.push_back(oc[r - 1]);
+      } else {
+        int pos = 0;
+        for (int d = 0; d < static_cast<int>(vals_[a].dims.size()); ++d) ac.push_back(d == cd[0] ? "kk" : oc[pos++]);
+        for (int d = 0; d < static_cast<int>(vals_[b].dims.size()); ++d) bc.push_back(d == cd[1] ? "kk" : oc[pos++]);
+      }
+      ln("float acc = 0.f;");
+      open("for (long long kk = 0; kk < " + std::to_string(K) + "LL; ++kk)");
+      memo_.emplace_back();
+      ln("acc = fmaf(" + at(a, ac) + ", " + at(b, bc) + ", acc);");
+      memo_.pop_back();
+      close();
+      ln(dst + "[i] = acc;");
+      spec_.flops += 2 * prod(v.dims) * K;
+    }
+    memo_.pop_back();
+    close();
+    materialized_[m] = v.output ? out_ptr(m) : "(ws + " + std::to_string(ws_off_[m]) + "LL)";
+  }
+}
+
+// ---------------------------------------------------------------------------
+// driver
+// ---------------------------------------------------------------------------
+
+KernelSpec Builder::build() {
+  collect();
+  spec_.name = name_;
+  std::vector<Component> comps = components();
+  bool sectioned = false;
+  for (Component& c : comps) {
+    if (plan_row(c)) continue;
+    if (all_elementwise(c)) {
+      c.scheme = "flat";
+      int64_t total = 0;
+      for (int o : c.outputs) total = std::max(total, prod(vals_[o].dims));
+      c.max_grid = std::max<int64_t>(1, (total / 4 + 255) / 256);
+      continue;
+    }
+    c.scheme = "sectioned";
+    sectioned = true;
+  }
+
+  // Block size: the widest CTA-mode row component, else 256.
+  int block = 256;
+  for (const Component& c : comps)
+    if (c.scheme == "row" && c.cta) block = std::max(block, c.NT);
+  for (Component& c : comps)
+    if (c.scheme == "row" && c.cta) c.NT = block;
+
+  std::ostringstream head;
+  std::string body_src;
+  int64_t smem_floats = 0;
+  if (sectioned) {
+    spec_.scheme = "sectioned";
+    spec_.cooperative = true;
+    spec_.composition = {"block"};
+    memo_.emplace_back();
+    indent_ = 1;
+    emit_sectioned(topo_members_);
+    memo_.pop_back();
+    body_src = out_.str();
+    int64_t maxe = 1;
+    for (int m : topo_members_) maxe = std::max(maxe, prod(vals_[m].dims));
+    spec_.max_grid = static_cast<int>(std::min<int64_t>((maxe + block - 1) / block, opts_.num_sms * 8));
+  } else {
+    // Workspace for cross-row partials: one row of partials per CTA.
+    const int64_t max_ctas = static_cast<int64_t>(opts_.num_sms) * 32;
+    bool coop = false;
+    for (Component& c : comps)
+      for (int x : c.cross) {
+        coop = true;
+        const OpNode& op = *vals_[x].node;
+        const int in = vals_[x].operands[0];
+        bool scalar = static_cast<int>(op.reduce_dims.size()) == static_cast<int>(vals_[in].dims.size());
+        const int64_t So = scalar ? 1 : prod(vals_[in].dims, c.k);
+        ws_off_[x] = ws_floats_;
+        ws_floats_ += max_ctas * ((So + 63) / 64 * 64);
+        if (!c.post.empty() && !vals_[x].output) {
+          int64_t off = ws_floats_;
+          ws_floats_ += (So + 63) / 64 * 64;
+          materialized_[x] = "(ws + " + std::to_string(off) + "LL)";
+        }
+      }
+    spec_.cooperative = coop;
+    // CTA ranges per component, proportional to weight.
+    int64_t total_w = 0;
+    for (const Component& c : comps) total_w += c.weight;
+    std::vector<std::string> lo(comps.size()), n(comps.size());
+    indent_ = 1;
+    if (comps.size() > 1) {
+      int64_t cum = 0;
+      ln("// kernel packing: " + std::to_string(comps.size()) + " independent components on disjoint CTA ranges");
+      std::vector<std::string> bounds;
+      for (size_t i = 0; i <= comps.size(); ++i) {
+        // b_i = max(i, floor(G * cum_i / W)), clipped so every component keeps a CTA
+        std::string b = "cb" + std::to_string(i);
+        if (i == 0) ln("const int cb0 = 0;");
+        else if (i == comps.size()) ln("const int " + b + " = gridDim.x;");
+        else
+          ln("const int " + b + " = max(cb" + std::to_string(i - 1) + " + 1, min((int)gridDim.x - " + std::to_string(comps.size() - i) +
+             ", (int)(((long long)gridDim.x * " + std::to_string(cum) + "LL) / " + std::to_string(total_w) + "LL)));");
+        if (i < comps.size()) cum += comps[i].weight;
+      }
+      for (size_t i = 0; i < comps.size(); ++i) {
+        lo[i] = "cb" + std::to_string(i);
+        n[i] = "(cb" + std::to_string(i + 1) + " - cb" + std::to_string(i) + ")";
+      }
+      spec_.composition.insert("packing");
+    } else {
+      lo[0] = "0";
+      n[0] = "gridDim.x";
+    }
+    std::vector<Component*> rowc;
+    std::string scheme;
+    for (size_t i = 0; i < comps.size(); ++i) {
+      Component& c = comps[i];
+      for (int x : c.cross) cross_parts_[x] = "(int)" + n[i];
+      if (comps.size() > 1) open("if ((int)blockIdx.x >= " + lo[i] + " && (int)blockIdx.x < cb" + std::to_string(i + 1) + ")");
+      memo_.emplace_back();
+      if (c.scheme == "row") {
+        emit_row(c, lo[i], n[i], "");
+        rowc.push_back(&c);
+        smem_floats = std::max(smem_floats, c.cta ? c.slab_floats + 32 + 4 : (c.slab_floats + 32) * (block / 32));
+        if (!c.cta)
+          for (int x : c.cross) {
+            const int in = vals_[x].operands[0];
+            smem_floats = std::max(smem_floats, (block / 32) * prod(vals_[in].dims, c.k));
+          }
+        spec_.composition.insert("thread");
+        bool has_red = false, has_block = c.cta;
+        for (int m : c.members) has_red = has_red || vals_[m].node->type == OpType::kReduce;
+        if (has_red && !c.cta) spec_.composition.insert("warp");
+        if (has_block) spec_.composition.insert("block");
+        std::ostringstream s;
+        s << (c.cta ? "row_cta" : "row_warp") << "(k=" << c.k << ",rows=" << c.R << ",nt=" << c.NT
+          << (c.tma ? ",tma" : "") << (c.cross.empty() ? "" : ",cross") << ")";
+        scheme += (scheme.empty() ? "" : "+") + s.str();
+        spec_.max_grid = std::max<int>(spec_.max_grid, static_cast<int>(std::min<int64_t>(c.max_grid, 1 << 20)));
+      } else {
+        emit_flat(c, lo[i], n[i]);
+        spec_.composition.insert("thread");
+        scheme += (scheme.empty() ? "" : "+") + std::string("flat");
+        spec_.max_grid = std::max<int>(spec_.max_grid, static_cast<int>(std::min<int64_t>(c.max_grid, 1 << 20)));
+      }
+      memo_.pop_back();
+      if (comps.size() > 1) close();
+    }
+    memo_.emplace_back();
+    emit_row_finalize(rowc);
+    memo_.pop_back();
+    spec_.max_grid = std::max<int>(spec_.max_grid, static_cast<int>(comps.size()));
+    spec_.scheme = scheme;
+    body_src = out_.str();
+  }
+
+  // Signature.
+  std::vector<std::string> params;
+  for (int v : inputs_) {
+    params.push_back("const float* __restrict__ " + in_ptr(v));
+    spec_.inputs.push_back(vals_[v].id);
+    spec_.algo_bytes += vals_[v].node->shape.byte_count();
+  }
+  for (int o : outputs_) {
+    params.push_back("float* __restrict__ " + out_ptr(o));
+    spec_.outputs.push_back(vals_[o].id);
+    spec_.algo_bytes += vals_[o].node->shape.byte_count();
+  }
+  params.push_back("float* __restrict__ ws");
+  params.push_back("unsigned int* __restrict__ gsync");
+  head << "// stitched kernel for fused op '" << name_ << "': " << topo_members_.size() << " ops, scheme "
+       << spec_.scheme << "\n";
+  for (int m : topo_members_) {
+    head << "//   " << vals_[m].id << " = " << to_string(vals_[m].node->type);
+    if (!vals_[m].node->elem_name.empty()) head << ":" << vals_[m].node->elem_name;
+    head << "(";
+    for (size_t i = 0; i < vals_[m].operands.size(); ++i) head << (i ? ", " : "") << vals_[vals_[m].operands[i]].id;
+    head << ")\n";
+  }
+  head << "extern \"C\" __global__ void __launch_bounds__(" << block << ") " << name_ << "(" << join(params, ", ")
+       << ") {\n";
+  head << "  extern __shared__ __align__(128) float smem[];\n";
+  head << "  (void)ws; (void)gsync; (void)smem;\n";
+  spec_.source = head.str() + body_src + "}\n";
+  spec_.block = block;
+  spec_.smem_bytes = static_cast<int>(smem_floats * 4 + (smem_floats ? 16 : 0));
+  spec_.workspace_floats = ws_floats_;
+  spec_.sync_words = (spec_.cooperative || uses_barrier_) ? 2 : 0;
+  if (uses_barrier_) spec_.cooperative = true;
+  if (spec_.max_grid < 1) spec_.max_grid = 1;
+  return spec_;
+}
+
+}  // namespace
+
+KernelSpec generate_kernel(const Graph& body, const std::string& name, const std::map<std::string, double>& constants,
+                           const CodegenOptions& opts) {
+  Builder b(body, name, constants, opts);
+  return b.build();
+}
+
+}  // namespace exec
+}  // namespace stitch

@@ -1,0 +1,62 @@
+// Stitched-kernel code generation: one fused op (its body graph) in, one
+// sm_100a CUDA kernel out. This replaces the reference's template search +
+// CUDA-C sketch emitter (proj/include/stitch/emitter.hpp) with kernels that
+// actually run: the paper's composition mechanisms (§5.1) become
+//
+//   ROW scheme   the group's tensors share a leading "row" index space; a
+//                warp (or a CTA) owns one row at a time and runs every fused
+//                op for it with intermediates in registers (thread
+//                composition), row reductions by shuffles (warp
+//                composition) or through shared memory plus TMA-staged
+//                operand tiles for gemm stages (block composition); column /
+//                scalar reductions accumulate per thread across rows and
+//                finish with a deterministic grid-wide combine;
+//   FLAT scheme  elementwise groups without a row structure: vectorised
+//                grid-stride loops;
+//   SECTIONED    the general fallback: one grid-stride section per
+//                materialised value, separated by a grid barrier;
+//   packing      independent components of one group run on disjoint CTA
+//                ranges of the same launch (§5.1(a)).
+#pragma once
+
+#include <cstdint>
+#include <map>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "../host/ir.hpp"
+
+namespace stitch {
+namespace exec {
+
+struct KernelSpec {
+  std::string name;
+  std::string source;  // generated kernel body; the device header is prepended at compile time
+  std::string scheme;  // human-readable scheme summary, e.g. "row_warp(k=1,S=768)"
+  std::set<std::string> composition;  // packing | thread | warp | block
+  int block = 256;
+  int max_grid = 1;          // useful CTAs; the runtime clamps cooperative grids to residency
+  bool cooperative = false;  // needs co-residency (grid barrier)
+  int smem_bytes = 0;        // dynamic shared memory per CTA
+  int64_t workspace_floats = 0;
+  int sync_words = 0;                // grid-barrier words
+  std::vector<std::string> inputs;   // pointer arguments, in order
+  std::vector<std::string> outputs;  // pointer arguments, in order
+  int64_t algo_bytes = 0;            // each input read once + each output written once
+  int64_t flops = 0;                 // 2*M*N*K summed over gemm stages
+};
+
+struct CodegenOptions {
+  int num_sms = 148;
+  int max_smem = 232448 - 1024;  // per-CTA opt-in limit minus a static-smem margin
+  bool allow_row = true;         // false forces SECTIONED (tests)
+};
+
+// `constants` maps body-parameter ids whose value is a known scalar constant
+// to that value; those become literals instead of pointer arguments.
+KernelSpec generate_kernel(const Graph& body, const std::string& name, const std::map<std::string, double>& constants,
+                           const CodegenOptions& opts = {});
+
+}  // namespace exec
+}  // namespace stitch

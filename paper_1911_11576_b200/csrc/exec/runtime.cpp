@@ -1,0 +1,531 @@
+// Stitched-kernel runtime (see runtime.hpp).
+#include "runtime.hpp"
+
+#include <nvrtc.h>
+
+#include <algorithm>
+#include <cctype>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <mutex>
+#include <sstream>
+#include <stdexcept>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include "cuda_api.hpp"
+
+namespace stitch {
+namespace exec {
+
+namespace {
+
+#include "device_header.inc"  // defines kDeviceHeader (generated from device/stitch_device.cuh)
+
+uint64_t fnv1a(const std::string& s) {
+  uint64_t h = 1469598103934665603ull;
+  for (unsigned char c : s) h = (h ^ c) * 1099511628211ull;
+  return h;
+}
+
+const char* kCompileOpts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "-DSTITCH_NVRTC=1"};
+
+std::string sanitize(const std::string& id) {
+  std::string s;
+  for (char c : id) s += (std::isalnum(static_cast<unsigned char>(c)) ? c : '_');
+  if (s.empty() || std::isdigit(static_cast<unsigned char>(s[0]))) s = "k_" + s;
+  return s;
+}
+
+std::mutex g_compile_mu;
+
+}  // namespace
+
+const std::string& device_header_source() {
+  static const std::string h(kDeviceHeader);
+  return h;
+}
+
+std::string full_source(const KernelSpec& spec) { return device_header_source() + "\n" + spec.source; }
+
+std::string compile_cubin(const std::string& source, const std::string& cache_dir, bool* cache_hit) {
+  std::string key = source;
+  for (const char* o : kCompileOpts) key += std::string("\n//opt ") + o;
+  char hex[32];
+  std::snprintf(hex, sizeof hex, "%016llx", static_cast<unsigned long long>(fnv1a(key)));
+  const std::string path = cache_dir.empty() ? "" : cache_dir + "/" + hex + ".cubin";
+  if (cache_hit) *cache_hit = false;
+  if (!path.empty()) {
+    std::ifstream in(path, std::ios::binary);
+    if (in) {
+      std::stringstream buf;
+      buf << in.rdbuf();
+      if (cache_hit) *cache_hit = true;
+      return buf.str();
+    }
+  }
+  std::lock_guard<std::mutex> lock(g_compile_mu);
+  nvrtcProgram prog;
+  if (nvrtcCreateProgram(&prog, source.c_str(), "stitched.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS)
+    throw std::runtime_error("nvrtcCreateProgram failed");
+  nvrtcResult rc = nvrtcCompileProgram(prog, static_cast<int>(sizeof(kCompileOpts) / sizeof(kCompileOpts[0])), kCompileOpts);
+  size_t log_size = 0;
+  nvrtcGetProgramLogSize(prog, &log_size);
+  std::string log(log_size, '\0');
+  if (log_size) nvrtcGetProgramLog(prog, &log[0]);
+  if (rc != NVRTC_SUCCESS) {
+    nvrtcDestroyProgram(&prog);
+    throw std::runtime_error(std::string("NVRTC compile failed: ") + nvrtcGetErrorString(rc) + "\n" + log);
+  }
+  size_t n = 0;
+  nvrtcGetCUBINSize(prog, &n);
+  std::string cubin(n, '\0');
+  nvrtcGetCUBIN(prog, &cubin[0]);
+  nvrtcDestroyProgram(&prog);
+  if (!path.empty()) {
+    mkdir(cache_dir.c_str(), 0755);
+    const std::string tmp = path + ".tmp" + std::to_string(getpid());
+    std::ofstream out(tmp, std::ios::binary);
+    out.write(cubin.data(), static_cast<std::streamsize>(cubin.size()));
+    out.close();
+    std::rename(tmp.c_str(), path.c_str());
+  }
+  return cubin;
+}
+
+// ---------------------------------------------------------------------------
+
+Executor::Executor(const Graph& fused, const ExecOptions& opts) : g_(fused), opts_(opts) {
+  for (const OpNode& n : g_.nodes)
+    if (n.type == OpType::kParameter || (n.type == OpType::kConstant && !n.value)) {
+      input_ids_.push_back(n.id);
+      input_dims_.push_back(n.shape.dims);
+      input_bytes_.push_back(n.shape.byte_count());
+      if (n.shape.dtype != DType::f32()) throw GraphError("stitched executor: only f32 inputs are supported (" + n.id + ")");
+    }
+  for (const std::string& o : g_.outputs) {
+    const OpNode& n = g_.at(o);
+    if (n.type == OpType::kTuple)
+      for (const std::string& e : n.operands) output_ids_.push_back(e);
+    else
+      output_ids_.push_back(o);
+  }
+  for (const std::string& o : output_ids_) {
+    output_dims_.push_back(g_.at(o).shape.dims);
+    output_bytes_.push_back(g_.at(o).shape.byte_count());
+  }
+  build_kernels();
+  plan_arena();
+  if (!opts_.compile_only) init_device();
+}
+
+Executor::~Executor() {
+  if (!device_ready_) return;
+  CudaApi& cu = CudaApi::get();
+  if (graph_exec_) cu.cuGraphExecDestroy(static_cast<CUgraphExec>(graph_exec_));
+  for (KernelInst& k : kernels_)
+    if (k.module) cu.cuModuleUnload(static_cast<CUmodule>(k.module));
+  if (arena_) cu.cuMemFree(arena_);
+  if (ws_) cu.cuMemFree(ws_);
+  if (sync_) cu.cuMemFree(sync_);
+  for (uint64_t p : host_staging_)
+    if (p) cu.cuMemFree(p);
+}
+
+void Executor::build_kernels() {
+  // Buffer key of a value id in the fused graph.
+  auto key_of = [&](const std::string& id) -> std::string {
+    const OpNode& n = g_.at(id);
+    if (n.type == OpType::kGetElement) return n.operands[0] + "#" + std::to_string(n.tuple_index);
+    if (n.type == OpType::kFused) return id + "#0";
+    return id;
+  };
+  std::map<std::string, int> input_slot;
+  for (size_t i = 0; i < input_ids_.size(); ++i) input_slot[input_ids_[i]] = static_cast<int>(i);
+  auto buffer = [&](const std::string& key, int64_t bytes) {
+    auto it = buf_of_.find(key);
+    if (it != buf_of_.end()) return it->second;
+    ValueBuf b;
+    b.key = key;
+    b.bytes = bytes;
+    auto s = input_slot.find(key);
+    if (s != input_slot.end()) {
+      b.kind = ValueBuf::kInput;
+      b.slot = s->second;
+    }
+    bufs_.push_back(b);
+    buf_of_[key] = static_cast<int>(bufs_.size()) - 1;
+    return static_cast<int>(bufs_.size()) - 1;
+  };
+
+  std::map<std::string, std::string> names;
+  for (const std::string& id : topological_sort(g_)) {
+    const OpNode& n = g_.at(id);
+    if (n.type != OpType::kFused && !is_fusible(n)) continue;
+    Graph body;
+    std::vector<std::string> outer_inputs;
+    std::vector<std::string> out_keys;
+    if (n.type == OpType::kFused) {
+      body = *n.body;
+      int p = 0;
+      for (const OpNode& bn : body.nodes)
+        if (bn.type == OpType::kParameter) outer_inputs.push_back(n.operands.at(p++));
+      const OpNode& tup = body.at(body.outputs.front());
+      for (size_t i = 0; i < tup.operands.size(); ++i) out_keys.push_back(id + "#" + std::to_string(i));
+    } else {
+      // Unfused kernel op: a one-op body, so it runs through the same generator.
+      for (const std::string& o : n.operands) {
+        if (body.contains(o)) continue;
+        OpNode prm;
+        prm.id = o;
+        prm.type = OpType::kParameter;
+        prm.shape = g_.at(o).shape;
+        body.add(prm);
+        outer_inputs.push_back(o);
+      }
+      body.add(n);
+      OpNode tup;
+      tup.id = "__outputs";
+      tup.type = OpType::kTuple;
+      tup.operands = {n.id};
+      tup.shape = n.shape;
+      body.add(tup);
+      body.outputs = {"__outputs"};
+      out_keys.push_back(id);
+    }
+    // Body parameter id -> outer value (positional for fused bodies).
+    std::map<std::string, std::string> outer_of;
+    std::map<std::string, double> consts;
+    int p = 0;
+    for (const OpNode& bn : body.nodes) {
+      if (bn.type != OpType::kParameter) continue;
+      const std::string& outer = outer_inputs.at(p++);
+      outer_of[bn.id] = outer;
+      const OpNode& on = g_.at(outer);
+      if (on.type == OpType::kConstant && on.value) consts[bn.id] = *on.value;
+    }
+    std::string kname = sanitize(id);
+    while (names.count(kname)) kname += "_";
+    names[kname] = id;
+    KernelInst k;
+    k.op_id = id;
+    k.spec = generate_kernel(body, kname, consts, opts_.codegen);
+    const OpNode& tup = body.at(body.outputs.front());
+    for (const std::string& in : k.spec.inputs) {
+      const std::string& outer = outer_of.at(in);
+      k.in_bufs.push_back(buffer(key_of(outer), g_.at(outer).shape.byte_count()));
+    }
+    for (const std::string& o : k.spec.outputs) {
+      auto pos = std::find(tup.operands.begin(), tup.operands.end(), o) - tup.operands.begin();
+      k.out_bufs.push_back(buffer(out_keys.at(pos), body.at(o).shape.byte_count()));
+    }
+    kernels_.push_back(std::move(k));
+  }
+  // Lifetimes.
+  for (size_t ki = 0; ki < kernels_.size(); ++ki) {
+    for (int b : kernels_[ki].out_bufs) {
+      if (bufs_[b].first >= 0) throw InternalError("value produced twice: " + bufs_[b].key);
+      bufs_[b].first = bufs_[b].last = static_cast<int>(ki);
+    }
+    for (int b : kernels_[ki].in_bufs) {
+      if (bufs_[b].kind == ValueBuf::kInput) continue;
+      if (bufs_[b].first < 0) throw InternalError("value consumed before it is produced: " + bufs_[b].key);
+      bufs_[b].last = std::max(bufs_[b].last, static_cast<int>(ki));
+    }
+  }
+  // Graph outputs.
+  for (size_t i = 0; i < output_ids_.size(); ++i) {
+    const OpNode& n = g_.at(output_ids_[i]);
+    std::string key = n.type == OpType::kGetElement ? n.operands[0] + "#" + std::to_string(n.tuple_index)
+                      : n.type == OpType::kFused    ? output_ids_[i] + "#0"
+                                                    : output_ids_[i];
+    auto it = buf_of_.find(key);
+    if (it == buf_of_.end() || bufs_[it->second].kind != ValueBuf::kArena) {
+      if (it == buf_of_.end()) throw GraphError("stitched executor: output " + output_ids_[i] + " is not computed by any kernel");
+      output_copies_.push_back({static_cast<int>(i), it->second});
+      continue;
+    }
+    bufs_[it->second].kind = ValueBuf::kOutput;
+    bufs_[it->second].slot = static_cast<int>(i);
+  }
+  // Compile (or fetch from the cache).
+  for (KernelInst& k : kernels_) {
+    bool hit = false;
+    std::string cubin = compile_cubin(full_source(k.spec), opts_.cache_dir, &hit);
+    k.cache_hit = hit;
+    k.module = nullptr;
+    k.spec.source.shrink_to_fit();
+    cubins_tmp_.push_back(std::move(cubin));
+  }
+}
+
+void Executor::plan_arena() {
+  std::vector<int> order;
+  for (size_t b = 0; b < bufs_.size(); ++b)
+    if (bufs_[b].kind == ValueBuf::kArena) order.push_back(static_cast<int>(b));
+  std::sort(order.begin(), order.end(), [&](int a, int b) { return bufs_[a].bytes > bufs_[b].bytes; });
+  std::vector<int> placed;
+  const int64_t align = 256;
+  for (int b : order) {
+    ValueBuf& x = bufs_[b];
+    std::vector<std::pair<int64_t, int64_t>> busy;
+    for (int p : placed) {
+      const ValueBuf& y = bufs_[p];
+      if (y.first <= x.last && x.first <= y.last) busy.push_back({y.offset, y.offset + y.bytes});
+    }
+    std::sort(busy.begin(), busy.end());
+    int64_t off = 0;
+    for (auto [lo, hi] : busy) {
+      if (off + x.bytes <= lo) break;
+      off = std::max(off, (hi + align - 1) / align * align);
+    }
+    x.offset = off;
+    arena_bytes_ = std::max(arena_bytes_, off + x.bytes);
+    placed.push_back(b);
+  }
+  for (KernelInst& k : kernels_) {
+    k.ws_off = 0;
+    ws_floats_ = std::max(ws_floats_, k.spec.workspace_floats);
+    k.sync_off = sync_words_;
+    sync_words_ += std::max(2, k.spec.sync_words) + 30;  // one 128-byte line per kernel
+  }
+}
+
+void Executor::init_device() {
+  CudaApi& cu = CudaApi::get();
+  cu_check(cu.cuInit(0), "cuInit");
+  CUcontext ctx = nullptr;
+  cu_check(cu.cuCtxGetCurrent(&ctx), "cuCtxGetCurrent");
+  CUdevice dev;
+  cu_check(cu.cuDeviceGet(&dev, opts_.device), "cuDeviceGet");
+  if (!ctx) {
+    cu_check(cu.cuDevicePrimaryCtxRetain(&ctx, dev), "cuDevicePrimaryCtxRetain");
+    cu_check(cu.cuCtxSetCurrent(ctx), "cuCtxSetCurrent");
+  }
+  cu_check(cu.cuDeviceGetAttribute(&sms_, CU_DEVICE_ATTRIBUTE_MULTIPROCESSOR_COUNT, dev), "sm count");
+  int major = 0, minor = 0;
+  cu.cuDeviceGetAttribute(&major, CU_DEVICE_ATTRIBUTE_COMPUTE_CAPABILITY_MAJOR, dev);
+  cu.cuDeviceGetAttribute(&minor, CU_DEVICE_ATTRIBUTE_COMPUTE_CAPABILITY_MINOR, dev);
+  if (major != 10 || minor != 0)
+    throw std::runtime_error("stitched executor kernels are built for sm_100a; device is sm_" + std::to_string(major) +
+                             std::to_string(minor));
+  CUdeviceptr p = 0;
+  cu_check(cu.cuMemAlloc(&p, std::max<int64_t>(arena_bytes_, 256)), "arena alloc");
+  arena_ = p;
+  cu_check(cu.cuMemAlloc(&p, std::max<int64_t>(ws_floats_ * 4, 256)), "workspace alloc");
+  ws_ = p;
+  cu_check(cu.cuMemAlloc(&p, std::max<int64_t>(sync_words_ * 4, 256)), "sync alloc");
+  sync_ = p;
+  cu_check(cu.cuMemsetD8Async(sync_, 0, std::max<int64_t>(sync_words_ * 4, 256), nullptr), "sync memset");
+  cu_check(cu.cuStreamSynchronize(nullptr), "sync");
+  for (size_t i = 0; i < kernels_.size(); ++i) {
+    KernelInst& k = kernels_[i];
+    CUmodule mod;
+    cu_check(cu.cuModuleLoadData(&mod, cubins_tmp_[i].data()), "cuModuleLoadData");
+    CUfunction fn;
+    cu_check(cu.cuModuleGetFunction(&fn, mod, k.spec.name.c_str()), "cuModuleGetFunction");
+    k.module = mod;
+    k.fn = fn;
+    if (k.spec.smem_bytes > 48 * 1024)
+      cu_check(cu.cuFuncSetAttribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, k.spec.smem_bytes),
+               "smem attribute");
+    int occ = 0;
+    cu_check(cu.cuOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, k.spec.block, k.spec.smem_bytes), "occupancy");
+    if (occ < 1) throw std::runtime_error("kernel " + k.spec.name + " cannot be resident (block/smem too large)");
+    const int64_t resident = static_cast<int64_t>(occ) * sms_;
+    k.grid = static_cast<int>(std::min<int64_t>(std::max(1, k.spec.max_grid), resident));
+    if (k.spec.cooperative) k.grid = static_cast<int>(std::min<int64_t>(k.grid, static_cast<int64_t>(sms_) * 32));
+  }
+  cubins_tmp_.clear();
+  device_ready_ = true;
+}
+
+void Executor::launch_all(const void* const* inputs, void* const* outputs, void* stream, std::vector<void*>* events) {
+  CudaApi& cu = CudaApi::get();
+  auto addr = [&](int b) -> CUdeviceptr {
+    const ValueBuf& x = bufs_[b];
+    if (x.kind == ValueBuf::kInput) return reinterpret_cast<CUdeviceptr>(inputs[x.slot]);
+    if (x.kind == ValueBuf::kOutput) return reinterpret_cast<CUdeviceptr>(outputs[x.slot]);
+    return arena_ + x.offset;
+  };
+  std::vector<CUdeviceptr> vals;
+  std::vector<void*> args;
+  for (size_t i = 0; i < kernels_.size(); ++i) {
+    KernelInst& k = kernels_[i];
+    vals.clear();
+    for (int b : k.in_bufs) vals.push_back(addr(b));
+    for (int b : k.out_bufs) vals.push_back(addr(b));
+    vals.push_back(ws_ + k.ws_off * 4);
+    vals.push_back(sync_ + k.sync_off * 4);
+    args.clear();
+    for (CUdeviceptr& v : vals) args.push_back(&v);
+    CUlaunchConfig cfg;
+    std::memset(&cfg, 0, sizeof cfg);
+    cfg.gridDimX = k.grid;
+    cfg.gridDimY = cfg.gridDimZ = 1;
+    cfg.blockDimX = k.spec.block;
+    cfg.blockDimY = cfg.blockDimZ = 1;
+    cfg.sharedMemBytes = k.spec.smem_bytes;
+    cfg.hStream = static_cast<CUstream>(stream);
+    CUlaunchAttribute attr[1];
+    if (k.spec.cooperative) {
+      attr[0].id = CU_LAUNCH_ATTRIBUTE_COOPERATIVE;
+      attr[0].value.cooperative = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+    }
+    if (events) cu_check(cu.cuEventRecord(static_cast<CUevent>((*events)[2 * i]), static_cast<CUstream>(stream)), "event");
+    cu_check(cu.cuLaunchKernelEx(&cfg, static_cast<CUfunction>(k.fn), args.data(), nullptr), k.spec.name.c_str());
+    if (events) cu_check(cu.cuEventRecord(static_cast<CUevent>((*events)[2 * i + 1]), static_cast<CUstream>(stream)), "event");
+  }
+  for (auto [slot, b] : output_copies_)
+    cu_check(cu.cuMemcpyDtoDAsync(reinterpret_cast<CUdeviceptr>(outputs[slot]), addr(b), output_bytes_[slot],
+                                  static_cast<CUstream>(stream)),
+             "output copy");
+}
+
+void Executor::run(const void* const* inputs, void* const* outputs, void* stream) {
+  if (!device_ready_) throw std::runtime_error("executor was created compile-only");
+  CudaApi& cu = CudaApi::get();
+  if (!opts_.use_graph || stream == nullptr) {
+    launch_all(inputs, outputs, stream, nullptr);
+    return;
+  }
+  std::vector<const void*> ptrs(inputs, inputs + input_ids_.size());
+  ptrs.insert(ptrs.end(), outputs, outputs + output_ids_.size());
+  if (!graph_exec_ || graph_stream_ != stream || ptrs != graph_ptrs_) {
+    if (graph_exec_) cu.cuGraphExecDestroy(static_cast<CUgraphExec>(graph_exec_));
+    graph_exec_ = nullptr;
+    cu_check(cu.cuStreamBeginCapture(static_cast<CUstream>(stream), CU_STREAM_CAPTURE_MODE_THREAD_LOCAL), "begin capture");
+    try {
+      launch_all(inputs, outputs, stream, nullptr);
+    } catch (...) {
+      CUgraph g = nullptr;
+      cu.cuStreamEndCapture(static_cast<CUstream>(stream), &g);
+      if (g) cu.cuGraphDestroy(g);
+      throw;
+    }
+    CUgraph graph = nullptr;
+    cu_check(cu.cuStreamEndCapture(static_cast<CUstream>(stream), &graph), "end capture");
+    CUgraphExec exec = nullptr;
+    cu_check(cu.cuGraphInstantiate(&exec, graph, 0), "graph instantiate");
+    cu.cuGraphDestroy(graph);
+    graph_exec_ = exec;
+    graph_stream_ = stream;
+    graph_ptrs_ = ptrs;
+  }
+  cu_check(cu.cuGraphLaunch(static_cast<CUgraphExec>(graph_exec_), static_cast<CUstream>(stream)), "graph launch");
+}
+
+void Executor::run_host(const void* const* host_inputs, void* const* host_outputs, void* stream) {
+  CudaApi& cu = CudaApi::get();
+  const size_t ni = input_ids_.size(), no = output_ids_.size();
+  if (host_staging_.empty()) {
+    host_staging_.resize(ni + no, 0);
+    for (size_t i = 0; i < ni + no; ++i) {
+      CUdeviceptr p;
+      cu_check(cu.cuMemAlloc(&p, std::max<int64_t>(i < ni ? input_bytes_[i] : output_bytes_[i - ni], 256)), "staging");
+      host_staging_[i] = p;
+    }
+  }
+  CUstream s = static_cast<CUstream>(stream);
+  std::vector<const void*> din(ni);
+  std::vector<void*> dout(no);
+  for (size_t i = 0; i < ni; ++i) {
+    cu_check(cu.cuMemcpyHtoDAsync(host_staging_[i], host_inputs[i], input_bytes_[i], s), "H2D");
+    din[i] = reinterpret_cast<const void*>(host_staging_[i]);
+  }
+  for (size_t i = 0; i < no; ++i) dout[i] = reinterpret_cast<void*>(host_staging_[ni + i]);
+  run(din.data(), dout.data(), stream);
+  for (size_t i = 0; i < no; ++i)
+    cu_check(cu.cuMemcpyDtoHAsync(host_outputs[i], host_staging_[ni + i], output_bytes_[i], s), "D2H");
+  cu_check(cu.cuStreamSynchronize(s), "stream sync");
+}
+
+json::Value Executor::profile(const void* const* inputs, void* const* outputs, void* stream, int iters) {
+  CudaApi& cu = CudaApi::get();
+  std::vector<void*> ev(2 * kernels_.size());
+  for (void*& e : ev) {
+    CUevent x;
+    cu_check(cu.cuEventCreate(&x, CU_EVENT_DEFAULT), "event create");
+    e = x;
+  }
+  std::vector<double> acc(kernels_.size(), 0.0);
+  for (int it = 0; it < std::max(1, iters); ++it) {
+    launch_all(inputs, outputs, stream, &ev);
+    cu_check(cu.cuStreamSynchronize(static_cast<CUstream>(stream)), "sync");
+    for (size_t i = 0; i < kernels_.size(); ++i) {
+      float ms = 0.f;
+      cu_check(cu.cuEventElapsedTime(&ms, static_cast<CUevent>(ev[2 * i]), static_cast<CUevent>(ev[2 * i + 1])), "elapsed");
+      acc[i] += ms;
+    }
+  }
+  for (void* e : ev) cu.cuEventDestroy(static_cast<CUevent>(e));
+  json::Value out = json::Value::object();
+  json::Value ks = json::Value::array();
+  double total = 0;
+  for (size_t i = 0; i < kernels_.size(); ++i) {
+    json::Value k = json::Value::object();
+    k.set("name", kernels_[i].spec.name);
+    k.set("op", kernels_[i].op_id);
+    double us = acc[i] * 1000.0 / std::max(1, iters);
+    k.set("us", us);
+    k.set("algo_bytes", kernels_[i].spec.algo_bytes);
+    k.set("gbps", us > 0 ? static_cast<double>(kernels_[i].spec.algo_bytes) / (us * 1e3) : 0.0);
+    total += us;
+    ks.push(k);
+  }
+  out.set("kernels", ks);
+  out.set("total_us", total);
+  return out;
+}
+
+json::Value Executor::describe() const {
+  json::Value j = json::Value::object();
+  auto tensors = [](const std::vector<std::string>& ids, const std::vector<std::vector<int64_t>>& dims,
+                    const std::vector<int64_t>& bytes) {
+    json::Value a = json::Value::array();
+    for (size_t i = 0; i < ids.size(); ++i) {
+      json::Value t = json::Value::object();
+      t.set("id", ids[i]);
+      t.set("dims", json::Value::array_of(dims[i]));
+      t.set("dtype", "f32");
+      t.set("bytes", bytes[i]);
+      a.push(t);
+    }
+    return a;
+  };
+  j.set("inputs", tensors(input_ids_, input_dims_, input_bytes_));
+  j.set("outputs", tensors(output_ids_, output_dims_, output_bytes_));
+  json::Value ks = json::Value::array();
+  int64_t algo = 0;
+  for (const KernelInst& k : kernels_) {
+    json::Value e = json::Value::object();
+    e.set("name", k.spec.name);
+    e.set("op", k.op_id);
+    e.set("scheme", k.spec.scheme);
+    json::Value comp = json::Value::array();
+    for (const std::string& c : k.spec.composition) comp.push(c);
+    e.set("composition", comp);
+    e.set("grid", k.grid);
+    e.set("block", k.spec.block);
+    e.set("smem_bytes", k.spec.smem_bytes);
+    e.set("cooperative", k.spec.cooperative);
+    e.set("algo_bytes", k.spec.algo_bytes);
+    e.set("flops", k.spec.flops);
+    e.set("inputs", json::Value::array_of(k.spec.inputs));
+    e.set("outputs", json::Value::array_of(k.spec.outputs));
+    e.set("cache_hit", k.cache_hit);
+    algo += k.spec.algo_bytes;
+    ks.push(e);
+  }
+  j.set("kernels", ks);
+  j.set("algo_bytes", algo);
+  j.set("arena_bytes", arena_bytes_);
+  j.set("workspace_bytes", ws_floats_ * 4);
+  return j;
+}
+
+}  // namespace exec
+}  // namespace stitch

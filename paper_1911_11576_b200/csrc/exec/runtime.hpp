@@ -1,0 +1,100 @@
+// Stitched-kernel runtime: NVRTC compilation to sm_100a cubins (with an
+// on-disk cache that build() pre-populates), an HBM arena for the values
+// crossing kernel boundaries, and the launch scheduler that replays the
+// fused graph's kernels in topological order -- directly or as one CUDA
+// graph. Replaces the reference's text-file codegen output
+// (proj/src/pipeline.cpp:99 run_codegen + tools/stitch_main.cpp cmd_codegen).
+#pragma once
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../host/ir.hpp"
+#include "../host/json.hpp"
+#include "codegen.hpp"
+
+namespace stitch {
+namespace exec {
+
+struct ExecOptions {
+  int device = 0;
+  std::string cache_dir;   // "" = no disk cache
+  bool use_graph = true;   // replay launches as a CUDA graph on non-null streams
+  bool compile_only = false;  // generate + compile, no device work (build-time cache fill)
+  CodegenOptions codegen;
+};
+
+const std::string& device_header_source();
+std::string full_source(const KernelSpec& spec);
+// NVRTC -> sm_100a cubin, through the disk cache when `cache_dir` is set.
+std::string compile_cubin(const std::string& source, const std::string& cache_dir, bool* cache_hit = nullptr);
+
+struct ValueBuf {
+  std::string key;
+  int64_t bytes = 0;
+  enum Kind { kInput, kOutput, kArena } kind = kArena;
+  int slot = -1;        // input / output position
+  int64_t offset = 0;   // arena byte offset
+  int first = -1, last = -1;  // producing / last consuming kernel
+};
+
+struct KernelInst {
+  KernelSpec spec;
+  std::string op_id;                 // fused op or unfused op id in the fused graph
+  std::vector<int> in_bufs, out_bufs;
+  void* module = nullptr;            // CUmodule
+  void* fn = nullptr;                // CUfunction
+  int grid = 1;
+  int64_t ws_off = 0;                // floats into the workspace pool
+  int64_t sync_off = 0;              // u32 words into the sync pool
+  bool cache_hit = false;
+};
+
+class Executor {
+ public:
+  Executor(const Graph& fused, const ExecOptions& opts);
+  ~Executor();
+  Executor(const Executor&) = delete;
+  Executor& operator=(const Executor&) = delete;
+
+  json::Value describe() const;
+  void run(const void* const* inputs, void* const* outputs, void* stream);
+  void run_host(const void* const* host_inputs, void* const* host_outputs, void* stream);
+  json::Value profile(const void* const* inputs, void* const* outputs, void* stream, int iters);
+
+  const std::vector<KernelInst>& kernels() const { return kernels_; }
+  const std::vector<std::string>& input_ids() const { return input_ids_; }
+  const std::vector<std::string>& output_ids() const { return output_ids_; }
+
+ private:
+  void build_kernels();
+  void plan_arena();
+  void init_device();
+  void launch_all(const void* const* inputs, void* const* outputs, void* stream, std::vector<void*>* events);
+
+  Graph g_;
+  ExecOptions opts_;
+  std::vector<ValueBuf> bufs_;
+  std::map<std::string, int> buf_of_;
+  std::vector<KernelInst> kernels_;
+  std::vector<std::string> input_ids_, output_ids_;
+  std::vector<int64_t> input_bytes_, output_bytes_;
+  std::vector<std::vector<int64_t>> input_dims_, output_dims_;
+  std::vector<std::pair<int, int>> output_copies_;  // (output slot, source buffer) when an output aliases another value
+  int64_t arena_bytes_ = 0, ws_floats_ = 0, sync_words_ = 0;
+  uint64_t arena_ = 0, ws_ = 0, sync_ = 0;  // CUdeviceptr
+  int sms_ = 148;
+  bool device_ready_ = false;
+  // CUDA-graph replay cache for the last pointer set
+  void* graph_exec_ = nullptr;
+  void* graph_stream_ = nullptr;
+  std::vector<const void*> graph_ptrs_;
+  std::vector<uint64_t> host_staging_;  // device buffers for run_host
+  std::vector<std::string> cubins_tmp_;  // compiled images until modules load
+};
+
+}  // namespace exec
+}  // namespace stitch

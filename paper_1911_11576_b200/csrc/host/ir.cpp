@@ -526,7 +526,10 @@ ContractResult contract_plan(const Graph& g, const std::vector<FusionPattern>& p
     pvert[i] = n + static_cast<int>(it - super_label.begin());
     if (it == super_label.end()) super_label.push_back(l);
   }
-  auto vtx = [&](int node) { return owner[node] < 0 ? node : pvert[owner[node]]; };
+  auto vtx = [&](int node) {
+    const int o = owner[node];
+    return o < 0 ? node : pvert.at(static_cast<size_t>(o));
+  };
   auto label = [&](int v) { return v < n ? g.nodes[v].id : super_label[v - n]; };
   const int nv = n + static_cast<int>(super_label.size());
   std::vector<int> order;  // vertices by first appearance in node order
