@@ -1,0 +1,457 @@
+"""Benchmark: fused-subgraph GB/s of the stitched executor on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl stitch|reference]
+
+One step = one pass of every BASELINE.json subgraph config (the suite in
+paper_1911_11576_b200/workloads.py, per-GPU batch shard each) through its
+fusion plan: one stitched sm_100a kernel per fusion group, launched by the
+C-ABI executor (CUDA-graph replay). Inputs are resident in HBM; L2 is flushed
+(256 MiB write) before every config, and the flush is outside the per-config
+CUDA-event intervals that make up the step time.
+
+value  = all ranks' algorithmic bytes (every subgraph input read once + every
+         output written once) / max-over-ranks step time, GB/s.
+e2e    = the same metric through stitch_executor_run_host (pinned host
+         buffers, H2D + run + D2H inside the timed region).
+unfused = the same suite with one kernel per op (the per-op CUDA baseline the
+         north star compares against); speedups per config and their geomean
+         are in config.suite.
+cpu_baseline = the oracle per-op interpreter (numpy fp32, 1 thread) on a
+         bounded sample, rank 0 at N=1.
+
+--impl reference: the reference's CPU path (the per-op oracle interpreter --
+the reference itself never executes graphs, SPEC fusion-transform
+Non-goals) on every host thread, on a bounded sample per step; rank 0 only.
+"""
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+PEAK_FALLBACK_GBS = 6650.0
+FLUSH_BYTES = 256 << 20
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="stitch", choices=["stitch", "reference"])
+    ap.add_argument("--configs", default="", help="comma-separated subset of the suite")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-unfused", action="store_true")
+    ap.add_argument("--out", default="", help="also write the JSON line to this file")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def suite_names(args):
+    from paper_1911_11576_b200 import workloads as W
+    names = list(W.CONFIGS)
+    if args.configs:
+        names = [n for n in args.configs.split(",") if n]
+    return names
+
+
+def graph_bytes(g):
+    from oracle import executor as orc  # shapes only
+    nodes = {n["id"]: n for n in g["nodes"]}
+    b = 0
+    for i in orc.graph_inputs(g):
+        b += 4 * int(np.prod(nodes[i]["shape"]["dims"]))
+    for o in orc.graph_outputs(g):
+        b += 4 * int(np.prod(nodes[o]["shape"]["dims"]))
+    return b
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy burst)"
+    except Exception:
+        return PEAK_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(kernel_name, config):
+    """dram bytes per launch of `kernel_name` from the committed ncu summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(config, {}).get(kernel_name)
+    except Exception:
+        return None
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q, "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                s, m = float(f[1]), float(f[2])
+            except ValueError:
+                continue
+            sm.append(s)
+            mx = max(mx, m)
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return None
+        load = sorted(sm)[len(sm) // 2:] if len(sm) > 2 else sm
+        return {"sm_mhz": float(np.median(load)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (oracle interpreter; test infrastructure used only as the baseline)
+# ---------------------------------------------------------------------------
+
+CPU_SAMPLE_DIV = {"layernorm": 16, "softmax": 16, "encoder": 32, "gru": 16}
+
+
+def _cpu_sample_graph(name, div):
+    from paper_1911_11576_b200 import workloads as W
+    fn = W.CONFIGS[name]
+    kw = {}
+    bk = W.BATCH_KW[name]
+    import inspect
+    full = inspect.signature(fn).parameters[bk].default
+    kw[bk] = max(1, full // div)
+    return fn(**kw), kw
+
+
+def cpu_oracle_gbps(names, threads, seconds_per_config):
+    """Oracle per-op interpreter (numpy fp32) over a batch sample of each
+    config, `threads` independent batch shards in parallel. Returns
+    (GB/s over the whole sample set, description)."""
+    from oracle import executor as orc
+    import concurrent.futures as cf
+    try:
+        from threadpoolctl import threadpool_limits
+    except Exception:  # pragma: no cover
+        threadpool_limits = None
+    total_b, total_t, desc = 0, 0.0, []
+    for name in names:
+        g, kw = _cpu_sample_graph(name, CPU_SAMPLE_DIV.get(name, 16))
+        ins = orc.random_inputs(g, seed=0)
+        b = graph_bytes(g)
+        ctx = threadpool_limits(1) if threadpool_limits else None
+
+        def one():
+            return orc.run(g, ins, dtype=np.float32)
+
+        reps = 0
+        t0 = time.perf_counter()
+        if ctx:
+            ctx.__enter__()
+        try:
+            if threads <= 1:
+                while True:
+                    one()
+                    reps += 1
+                    if time.perf_counter() - t0 >= seconds_per_config:
+                        break
+            else:
+                with cf.ThreadPoolExecutor(threads) as pool:
+                    while True:
+                        list(pool.map(lambda _: one(), range(threads)))
+                        reps += threads
+                        if time.perf_counter() - t0 >= seconds_per_config:
+                            break
+        finally:
+            if ctx:
+                ctx.__exit__(None, None, None)
+        dt = time.perf_counter() - t0
+        total_b += b * reps
+        total_t += dt
+        desc.append("%s %s x%d" % (name, ",".join("%s=%d" % kv for kv in kw.items()), reps))
+    return total_b / total_t / 1e9, "; ".join(desc)
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the per-op CPU interpreter on every host thread."""
+    if rank != 0:
+        return
+    names = suite_names(args)
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except Exception:
+        cores = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_oracle_gbps(names, cores, 0.0)
+    vals = []
+    sample = ""
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        v, sample = cpu_oracle_gbps(names, cores, 0.0)
+        vals.append(v)
+    wall = time.perf_counter() - t0
+    value = float(np.mean(vals))
+    line = {
+        "impl": "reference", "metric": "fused-subgraph GB/s", "value": value, "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": wall * 1e3 / max(1, args.steps), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "suite:" + ",".join(names) + " (per-step CPU sample)", "parallelism": "host threads"},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": cores, "kind": "port",
+                         "sample": "oracle per-op numpy fp32 interpreter, one batch shard per thread: " + sample},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    emit(line, args)
+
+
+def emit(line, args):
+    s = json.dumps(line)
+    print(s, flush=True)
+    if args.out:
+        with open(args.out, "w") as f:
+            f.write(s + "\n")
+
+
+# ---------------------------------------------------------------------------
+# GPU leg
+# ---------------------------------------------------------------------------
+
+def main():
+    args = parse_args()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_1911_11576_b200 import runtime as rt
+    from paper_1911_11576_b200 import workloads as W
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(device=dev)
+    sh = stream.cuda_stream
+    names = suite_names(args)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+
+    cfgs = []
+    for name in names:
+        g = W.CONFIGS[name]()
+        t0 = time.perf_counter()
+        plan = rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT)
+        plan_ms = (time.perf_counter() - t0) * 1e3
+        ex = rt.Executor(plan["fused"], device=local)
+        base = None if args.no_unfused else rt.Executor(g, device=local)
+        ins = [torch.randn(t["dims"], device=dev, generator=gen, dtype=torch.float32) for t in ex.info["inputs"]]
+        outs = [torch.empty(t["dims"], device=dev, dtype=torch.float32) for t in ex.info["outputs"]]
+        outs_b = [torch.empty_like(o) for o in outs] if base else None
+        cfgs.append(dict(name=name, g=g, ex=ex, base=base, ins=ins, outs=outs, outs_b=outs_b,
+                         bytes=graph_bytes(g), plan_ms=plan_ms,
+                         groups=sum(1 for n in plan["fused"]["nodes"] if n["kind"] == "fused"),
+                         kernels=len(ex.info["kernels"])))
+    flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
+
+    def timed_pass(which, ev_pairs):
+        with torch.cuda.stream(stream):
+            for i, c in enumerate(cfgs):
+                flush.zero_()
+                ev_pairs[i][0].record(stream)
+                if which == "fused":
+                    c["ex"].run(c["ins"], c["outs"], stream=sh)
+                else:
+                    c["base"].run(c["ins"], c["outs_b"], stream=sh)
+                ev_pairs[i][1].record(stream)
+
+    def measure(which, steps, warmup, clocks=None):
+        evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in cfgs]
+               for _ in range(steps)]
+        for _ in range(warmup):
+            timed_pass(which, [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                               for _ in cfgs])
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        if clocks:
+            clocks.start()
+        for s in range(steps):
+            timed_pass(which, evs[s])
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ck = clocks.stop() if clocks else None
+        per_cfg = np.zeros(len(cfgs))
+        for s in range(steps):
+            for i in range(len(cfgs)):
+                per_cfg[i] += evs[s][i][0].elapsed_time(evs[s][i][1])
+        per_cfg /= steps  # ms per config per step
+        t = torch.tensor(per_cfg, dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.cpu().numpy(), ck
+
+    clocks = Clocks(local)
+    fused_ms, ck = measure("fused", args.steps, max(3, args.warmup), clocks)
+    base_ms = None
+    if not args.no_unfused:
+        base_ms, _ = measure("unfused", args.steps, max(3, args.warmup))
+
+    total_bytes = sum(c["bytes"] for c in cfgs)
+    step_ms = float(fused_ms.sum())
+    value = world * total_bytes / (step_ms * 1e-3) / 1e9
+
+    # Dominant kernel: per-launch CUDA events on the launching stream, L2
+    # flushed before every pass (stitch_executor_profile).
+    peak, peak_src = measured_peak()
+    best = None
+    kstats = {}
+    for c in cfgs:
+        acc = {}
+        reps = max(3, min(10, args.steps))
+        for _ in range(reps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            prof = c["ex"].profile(c["ins"], c["outs"], stream=sh, iters=1)
+            for k in prof["kernels"]:
+                acc.setdefault(k["name"], [0.0, k["algo_bytes"]])[0] += k["us"] / reps
+        kstats[c["name"]] = acc
+        for kname, (us, ab) in acc.items():
+            if best is None or us > best[2]:
+                best = (c["name"], kname, us, ab)
+    suite = {}
+    speedups = []
+    for i, c in enumerate(cfgs):
+        gbps = c["bytes"] / (fused_ms[i] * 1e-3) / 1e9
+        e = {"GBps": round(gbps, 1), "frac_of_hbm": round(gbps / peak, 3), "ms": round(float(fused_ms[i]), 4),
+             "algo_bytes": c["bytes"], "fusion_groups": c["groups"], "kernels": c["kernels"],
+             "plan_ms": round(c["plan_ms"], 1),
+             "kernel_us": {k: round(v[0], 2) for k, v in kstats[c["name"]].items()},
+             "kernel_frac_of_hbm": {k: round(v[1] / (v[0] * 1e-6) / 1e9 / peak, 3) for k, v in kstats[c["name"]].items()}}
+        if base_ms is not None:
+            sp = float(base_ms[i] / fused_ms[i])
+            e.update({"unfused_GBps": round(c["bytes"] / (base_ms[i] * 1e-3) / 1e9, 1),
+                      "unfused_kernels": len(c["base"].info["kernels"]), "speedup_vs_unfused": round(sp, 3)})
+            speedups.append(sp)
+        suite[c["name"]] = e
+    geo = float(math.exp(np.mean(np.log(speedups)))) if speedups else None
+
+    # End to end through the public C-ABI entry with host buffers.
+    e2e = None
+    if not args.no_e2e:
+        hin = [[x.cpu().pin_memory() for x in c["ins"]] for c in cfgs]
+        hout = [[torch.empty(o.shape, dtype=o.dtype).pin_memory() for o in c["outs"]] for c in cfgs]
+        h2d = sum(x.numel() * 4 for c in cfgs for x in c["ins"])
+        d2h = sum(x.numel() * 4 for c in cfgs for x in c["outs"])
+        for _ in range(2):
+            for i, c in enumerate(cfgs):
+                c["ex"].run_host(hin[i], hout[i], stream=sh)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        reps = max(3, min(args.steps, 10))
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(reps):
+            for i, c in enumerate(cfgs):
+                c["ex"].run_host(hin[i], hout[i], stream=sh)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = torch.tensor([ev0.elapsed_time(ev1) / reps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * total_bytes / (float(e2e_ms.item()) * 1e-3) / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": float(e2e_ms.item())}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, sample = cpu_oracle_gbps(names, 1, 2.0)
+        cpu = {"value": v, "unit": "GB/s", "cores": 1, "kind": "port",
+               "sample": "oracle per-op numpy fp32 interpreter, 1 thread: " + sample}
+
+    cfg_name, kname, kus, kbytes = best
+    achieved = kbytes / (kus * 1e-6) / 1e9
+    line = {
+        "metric": "fused-subgraph GB/s", "value": value, "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": step_ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (randn inputs resident in HBM)",
+        "config": {
+            "workload": "suite:" + ",".join(names) + " (BASELINE.json configs, per-GPU batch shard each)",
+            "parallelism": "batch-sharded dp%d, no collectives" % world,
+            "l2": "flushed (256 MiB write) before every config; flush outside the timed CUDA-event intervals",
+            "shared_limit_bytes": W.B200_SHARED_LIMIT,
+            "geomean_speedup_vs_unfused": geo,
+            "suite": suite,
+        },
+        "roofline": {"bound": "hbm", "kernel": "%s/%s" % (cfg_name, kname), "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_src,
+                     "traffic": ncu_traffic(kname, cfg_name), "algo_bytes_per_launch": kbytes,
+                     "us_per_launch": kus},
+        "gpu_launches": int(args.steps * sum(c["kernels"] for c in cfgs)),
+    }
+    if ck:
+        line["clocks"] = ck
+    if e2e:
+        line["e2e"] = e2e
+    if cpu:
+        line["cpu_baseline"] = cpu
+    if rank == 0:
+        emit(line, args)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,193 @@
+"""Test infrastructure (oracle) -- the stated fp32 tolerance.
+
+NOT part of the product: only tests/, __graft_entry__.smoke() and bench.py's
+checker legs import this module.
+
+The stitched kernels compute in fp32; the oracle (oracle/executor.py)
+computes in fp64. The acceptance rule (BASELINE.json north_star) is
+"within 1e-5 relative or 1e-6 absolute, with the reduction-order tolerance
+stated". This module states that tolerance per element:
+
+    |got - ref| <= max(RTOL * |ref|, ATOL) + SAFETY * bound
+
+where `bound` is a first-order forward rounding-error bound of evaluating the
+same graph in fp32 (unit roundoff u = 2^-24) in ANY summation order:
+
+    parameter        0 (inputs are exact fp32 values)
+    constant         u |c|                  (the literal is rounded to fp32)
+    a +- b           ea + eb + u |r|
+    a * b            |b| ea + |a| eb + ea eb + u |r|
+    a / b            (ea + |r| eb) / (|b| - eb) + u |r|      (inf if |b| <= eb)
+    exp(a)           |r| (exp(ea) - 1) + 2u |r|             (expf: <= 2 ulp)
+    log(a)           ea / (|a| - ea) + 2u |r|               (logf: <= 2 ulp)
+    rsqrt(a)         |r| (1/sqrt(1 - ea/|a|) - 1) + 2u |r|  (rsqrtf: <= 2 ulp)
+    negate/broadcast ea (exact)
+    max / min        max(ea, eb)
+    compare          1 where |a - b| <= ea + eb (the predicate may flip), else 0
+    select           e of the chosen branch; |a - b| + ea + eb where the
+                     predicate itself is uncertain
+    sum over n       sum e_i + (n - 1) u sum |x_i|   <- the reduction-order
+                     term: the classic worst case over every association
+                     (sequential, shuffle trees, blocked and cross-CTA
+                     combines alike)
+    max reduce       max e_i (exact)
+    dot (K terms)    |A| eB + eA |B| + K u |A||B|
+
+The fp64 oracle's own error is far below these bounds. SAFETY = 2 covers the
+dropped second-order terms.
+"""
+
+import numpy as np
+
+from . import executor as orc
+
+U = 2.0 ** -24
+RTOL = 1e-5
+ATOL = 1e-6
+SAFETY = 2.0
+
+
+def _eval(node, vals, errs, inputs):
+    kind = node["kind"]
+    dims = list(node["shape"]["dims"])
+    ops = node.get("operands", [])
+    a = [vals[o] for o in ops]
+    e = [errs[o] for o in ops]
+    if kind == "parameter":
+        v = np.asarray(inputs[node["id"]], dtype=np.float64).reshape(dims)
+        return v, np.zeros_like(v)
+    if kind == "constant":
+        if "value" in node:
+            v = np.full(dims, node["value"], dtype=np.float64)
+        else:
+            v = np.asarray(inputs[node["id"]], dtype=np.float64).reshape(dims)
+        return v, U * np.abs(v)
+    if kind == "tuple":
+        return list(a), list(e)
+    if kind == "elementwise":
+        name = node["name"]
+        if name == "broadcast":
+            return (np.ascontiguousarray(orc._broadcast(a[0], dims)),
+                    np.ascontiguousarray(orc._broadcast(e[0], dims)))
+        with np.errstate(all="ignore"):
+            r = np.asarray(orc._elementwise(name, a, dims, np.float64), dtype=np.float64).reshape(dims)
+            ar = np.abs(r)
+            if name in ("add", "subtract"):
+                err = e[0] + e[1] + U * ar
+            elif name == "multiply":
+                err = np.abs(a[1]) * e[0] + np.abs(a[0]) * e[1] + e[0] * e[1] + U * ar
+            elif name == "divide":
+                den = np.abs(a[1]) - e[1]
+                err = np.where(den > 0, (e[0] + ar * e[1]) / np.where(den > 0, den, 1.0), np.inf) + U * ar
+            elif name == "exp":
+                err = ar * np.expm1(e[0]) + 2 * U * ar
+            elif name == "log":
+                den = np.abs(a[0]) - e[0]
+                err = np.where(den > 0, e[0] / np.where(den > 0, den, 1.0), np.inf) + 2 * U * ar
+            elif name == "rsqrt":
+                q = e[0] / np.abs(a[0])
+                err = np.where(q < 1, ar * (1.0 / np.sqrt(np.maximum(1 - q, 1e-300)) - 1.0), np.inf) + 2 * U * ar
+            elif name == "negate":
+                err = e[0].copy()
+            elif name in ("maximum", "minimum"):
+                err = np.maximum(e[0], e[1])
+            elif name == "compare":
+                err = (np.abs(a[0] - a[1]) <= e[0] + e[1]).astype(np.float64)
+            elif name == "select":
+                unsure = np.abs(a[0]) <= e[0]
+                chosen = np.where(a[0] != 0, e[1], e[2])
+                err = np.where(unsure, np.abs(a[1] - a[2]) + e[1] + e[2], chosen)
+            else:
+                raise ValueError("unknown elementwise op " + name)
+        return r, err
+    if kind == "reduce":
+        axes = tuple(node["reduce_dims"])
+        if node.get("name") == "max":
+            return np.max(a[0], axis=axes).reshape(dims), np.max(e[0], axis=axes).reshape(dims)
+        n = int(np.prod([a[0].shape[d] for d in axes]))
+        v = np.sum(a[0], axis=axes).reshape(dims)
+        err = (np.sum(e[0], axis=axes) + (n - 1) * U * np.sum(np.abs(a[0]), axis=axes)).reshape(dims)
+        return v, err
+    if kind in ("dot", "batched_dot"):
+        A, B, eA, eB = a[0], a[1], e[0], e[1]
+        if kind == "dot":
+            cd = node.get("contract_dims")
+            if cd is None or cd[0] < 0:
+                cd = [A.ndim - 1, max(0, B.ndim - 2)]
+            K = A.shape[cd[0]]
+            mm = lambda x, y: np.tensordot(x, y, axes=([cd[0]], [cd[1]]))
+        else:
+            K = A.shape[-1]
+            mm = np.matmul
+        v = mm(A, B).reshape(dims)
+        err = (mm(np.abs(A), eB) + mm(eA, np.abs(B)) + K * U * mm(np.abs(A), np.abs(B))).reshape(dims)
+        return v, err
+    if kind == "get_element":
+        return a[0][node["index"]], e[0][node["index"]]
+    if kind == "fused":
+        body = node["body"]
+        params = [n["id"] for n in body["nodes"] if n["kind"] == "parameter"]
+        bv, be = _evaluate(body, dict(zip(params, a)), dict(zip(params, e)))
+        out = body["outputs"][0]
+        return bv[out], be[out]
+    raise ValueError("unknown op kind " + kind)
+
+
+def _evaluate(graph, inputs, input_errs=None):
+    vals, errs = {}, {}
+    nodes = {n["id"]: n for n in graph["nodes"]}
+    order = []
+    seen = set()
+
+    def visit(nid):
+        stack = [(nid, False)]
+        while stack:
+            cur, done = stack.pop()
+            if done:
+                order.append(cur)
+                continue
+            if cur in seen:
+                continue
+            seen.add(cur)
+            stack.append((cur, True))
+            for o in nodes[cur].get("operands", []):
+                if o not in seen:
+                    stack.append((o, False))
+
+    for n in graph["nodes"]:
+        visit(n["id"])
+    for nid in order:
+        node = nodes[nid]
+        if input_errs is not None and node["kind"] == "parameter":
+            vals[nid] = np.asarray(inputs[nid], dtype=np.float64)
+            errs[nid] = np.asarray(input_errs[nid], dtype=np.float64)
+            continue
+        vals[nid], errs[nid] = _eval(node, vals, errs, inputs)
+    return vals, errs
+
+
+def reference_with_bound(graph, inputs):
+    """(outputs, bounds): the fp64 oracle outputs of `graph` (flattened
+    through tuples, executor output order) and the fp32 forward error bound
+    of each."""
+    vals, errs = _evaluate(graph, inputs)
+    outs = orc.graph_outputs(graph)
+    return [vals[o] for o in outs], [errs[o] for o in outs]
+
+
+def check(got, ref, bound):
+    """(ok, worst): worst = max |got - ref| / tol over elements (<= 1 passes).
+    NaN matches NaN; infinities must match exactly."""
+    got = np.asarray(got, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    if got.shape != ref.shape:
+        got = got.reshape(ref.shape)
+    tol = np.maximum(RTOL * np.abs(ref), ATOL) + SAFETY * np.asarray(bound, dtype=np.float64)
+    both_nan = np.isnan(got) & np.isnan(ref)
+    same_inf = np.isinf(ref) & (got == ref)
+    with np.errstate(invalid="ignore"):
+        ratio = np.abs(got - ref) / tol
+    ratio = np.where(both_nan | same_inf, 0.0, ratio)
+    ratio = np.where(np.isnan(ratio), np.inf, ratio)
+    worst = float(ratio.max()) if ratio.size else 0.0
+    return worst <= 1.0, worst

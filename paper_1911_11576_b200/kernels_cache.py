@@ -1,0 +1,40 @@
+"""Build-time fill of the in-tree kernel cache (paper_1911_11576_b200/_kcache).
+
+Every stitched kernel the benchmark and the GPU parity tests launch is
+generated and compiled to an sm_100a cubin by NVRTC here (no GPU needed), so
+the GPU box loads cubins instead of compiling. The cache is keyed by the
+FNV-1a hash of the full kernel source plus the NVRTC options
+(exec/runtime.cpp compile_cubin); a miss on the box just compiles there.
+"""
+
+from . import runtime as rt
+from . import workloads as W
+
+
+def plans(full=True, small=True):
+    """(tag, fused graph) for every plan bench.py and tests/ execute."""
+    out = []
+    for name, fn in W.CONFIGS.items():
+        sizes = []
+        if full:
+            sizes.append(("full", {}))
+        if small:
+            sizes.append(("small", W.SMALL[name]))
+        for size, kw in sizes:
+            g = fn(**kw)
+            for lim_tag, lim in (("b200", W.B200_SHARED_LIMIT), ("ref48k", W.REFERENCE_SHARED_LIMIT)):
+                out.append(("%s/%s/%s" % (name, size, lim_tag), rt.plan(g, shared_limit_bytes=lim)["fused"]))
+            out.append(("%s/%s/unfused" % (name, size), g))
+    return out
+
+
+def prebuild(verbose=True):
+    n = hits = 0
+    for tag, fused in plans():
+        ex = rt.Executor(fused, compile_only=True)
+        for k in ex.info["kernels"]:
+            n += 1
+            hits += bool(k["cache_hit"])
+        ex.close()
+    if verbose:
+        print("kernel cache: %d kernels (%d already cached) in %s" % (n, hits, rt.CACHE_DIR))

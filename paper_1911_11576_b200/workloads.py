@@ -225,3 +225,188 @@ CONFIGS = {
     "encoder": encoder,
     "gru": gru,
 }
+
+
+# ---------------------------------------------------------------------------
+# configs[4]: the memory-intensive ops of a BERT-base training step
+# ---------------------------------------------------------------------------
+
+B200_SHARED_LIMIT = 232448  # 227 KiB: the per-CTA opt-in shared memory of an sm_100a SM
+REFERENCE_SHARED_LIMIT = 49152  # the reference's default T (SPEC cost-model CostConfig)
+
+
+def _cbcast(g, id, value, dims):
+    return g.bcast(id + "_b", g.const(id, value), dims)
+
+
+def _layernorm_bwd(g, dy, x, lead, C, pre, gamma, eps=1e-5):
+    """Row LayerNorm backward from the saved LN input x (mean / rstd
+    recomputed): returns (dx, dgamma, dbeta).
+        xhat = (x - mean) * rstd,  gd = dy * gamma
+        dx = rstd * (gd - mean(gd) - xhat * mean(gd * xhat))
+        dgamma = sum_rows(dy * xhat),  dbeta = sum_rows(dy)"""
+    full = list(lead) + [C]
+    rdim = [len(lead)]
+    cdims = list(range(len(lead)))
+    inv = _cbcast(g, pre + "inv_n", 1.0 / C, lead)
+    epsb = _cbcast(g, pre + "eps", eps, lead)
+    s = g.reduce(pre + "sum", x, rdim, lead)
+    mean = g.ew(pre + "mean", "multiply", [s, inv], lead)
+    xc = g.ew(pre + "xc", "subtract", [x, g.bcast(pre + "mean_b", mean, full)], full)
+    sq = g.ew(pre + "sq", "multiply", [xc, xc], full)
+    var = g.ew(pre + "var", "multiply", [g.reduce(pre + "var_sum", sq, rdim, lead), inv], lead)
+    rs = g.ew(pre + "rstd", "rsqrt", [g.ew(pre + "var_eps", "add", [var, epsb], lead)], lead)
+    rb = g.bcast(pre + "rstd_b", rs, full)
+    xhat = g.ew(pre + "xhat", "multiply", [xc, rb], full)
+    gd = g.ew(pre + "gd", "multiply", [dy, g.bcast(pre + "gamma_b", gamma, full)], full)
+    m1 = g.ew(pre + "m1", "multiply", [g.reduce(pre + "gd_sum", gd, rdim, lead), inv], lead)
+    gx = g.ew(pre + "gx", "multiply", [gd, xhat], full)
+    m2 = g.ew(pre + "m2", "multiply", [g.reduce(pre + "gx_sum", gx, rdim, lead), inv], lead)
+    t1 = g.ew(pre + "t1", "subtract", [gd, g.bcast(pre + "m1_b", m1, full)], full)
+    t2 = g.ew(pre + "t2", "multiply", [xhat, g.bcast(pre + "m2_b", m2, full)], full)
+    t3 = g.ew(pre + "t3", "subtract", [t1, t2], full)
+    dx = g.ew(pre + "dx", "multiply", [t3, rb], full)
+    dyx = g.ew(pre + "dyx", "multiply", [dy, xhat], full)
+    dgamma = g.reduce(pre + "dgamma", dyx, cdims, [C])
+    dbeta = g.reduce(pre + "dbeta", dy, cdims, [C])
+    return dx, dgamma, dbeta
+
+
+def _gelu_bwd(g, dout, x, dims, pre):
+    """d/dx of x * s(z), s = sigmoid, z = k (x + a x^3), k = 2 sqrt(2/pi):
+        s + x s (1 - s) k (1 + 3 a x^2)."""
+    k = _cbcast(g, pre + "k", 2.0 * math.sqrt(2.0 / math.pi), dims)
+    a = _cbcast(g, pre + "a", 0.044715, dims)
+    a3 = _cbcast(g, pre + "a3", 3.0 * 0.044715, dims)
+    one = _cbcast(g, pre + "one", 1.0, dims)
+    x2 = g.ew(pre + "x2", "multiply", [x, x], dims)
+    x3 = g.ew(pre + "x3", "multiply", [x2, x], dims)
+    inner = g.ew(pre + "inner", "add", [x, g.ew(pre + "ax3", "multiply", [a, x3], dims)], dims)
+    z = g.ew(pre + "z", "multiply", [k, inner], dims)
+    ez = g.ew(pre + "ez", "exp", [g.ew(pre + "nz", "negate", [z], dims)], dims)
+    s = g.ew(pre + "s", "divide", [one, g.ew(pre + "den", "add", [one, ez], dims)], dims)
+    oms = g.ew(pre + "oms", "subtract", [one, s], dims)
+    zp = g.ew(pre + "zp", "multiply", [k, g.ew(pre + "zp1", "add", [one, g.ew(pre + "a3x2", "multiply", [a3, x2], dims)], dims)], dims)
+    t = g.ew(pre + "t", "multiply", [g.ew(pre + "xs", "multiply", [x, s], dims), oms], dims)
+    dgl = g.ew(pre + "dgelu", "add", [s, g.ew(pre + "tz", "multiply", [t, zp], dims)], dims)
+    return g.ew(pre + "dx", "multiply", [dout, dgl], dims)
+
+
+def bert(layers=12, batch=32, seq=128, hidden=768, heads=12, inter=3072):
+    """configs[4]: every memory-intensive op of one BERT-base training step
+    (forward and backward of `layers` encoder layers). GEMM / batched-GEMM
+    results and the activations the backward pass reads are graph
+    parameters (those GEMMs are partition ops the planner never fuses --
+    reference multi-step heuristic, pattern_gen.cpp -- and run in cuBLAS in a
+    real step); everything between them is planned and stitched:
+
+      forward   QKV bias; scaled + masked softmax; attention-output bias +
+                residual + LayerNorm; FFN bias + GeLU; FFN bias + residual +
+                LayerNorm
+      backward  LayerNorm backward (row reductions) with dgamma / dbeta and
+                bias gradients (column reductions); GeLU backward; softmax
+                backward; residual-gradient sums
+
+    Rows are tokens (batch * seq) or attention rows (batch * heads * seq):
+    the batch shards across GPUs with no exchange (bias / LN parameter
+    gradients are per-shard partials, summed by the optimizer's all-reduce
+    outside this subgraph)."""
+    g = GraphBuilder()
+    T = batch * seq
+    RA = batch * heads * seq
+    H, I = hidden, inter
+    tok = [T, H]
+    mask = g.param("mask", [seq])
+    x = g.param("emb", tok)
+    outs = []
+    for l in range(layers):
+        p = "f%d_" % l
+        qkv = g.ew(p + "qkv", "add", [g.param(p + "qkv_mm", [T, 3 * H]),
+                                      g.bcast(p + "bqkv_b", g.param(p + "bqkv", [3 * H]), [T, 3 * H])], [T, 3 * H])
+        outs.append(qkv)
+        sc = [RA, seq]
+        xs = g.ew(p + "xs", "multiply", [g.param(p + "scores", sc), _cbcast(g, p + "scale", 1.0 / math.sqrt(H / heads), sc)], sc)
+        xm = g.ew(p + "xm", "add", [xs, g.bcast(p + "mask_b", mask, sc)], sc)
+        outs.append(_softmax_rows(g, xm, [RA], seq, p + "sm_"))
+        ao = g.ew(p + "ao", "add", [g.param(p + "ao_mm", tok), g.bcast(p + "bo_b", g.param(p + "bo", [H]), tok)], tok)
+        r1 = g.ew(p + "r1", "add", [ao, x], tok)
+        ln1 = _layernorm(g, r1, [T], H, p + "ln1_", g.param(p + "g1", [H]), g.param(p + "be1", [H]))
+        outs.append(ln1)
+        ff = [T, I]
+        f1 = g.ew(p + "f1", "add", [g.param(p + "f1_mm", ff), g.bcast(p + "b1_b", g.param(p + "b1", [I]), ff)], ff)
+        outs.append(_gelu(g, f1, ff, p + "gl_"))
+        f2 = g.ew(p + "f2", "add", [g.param(p + "f2_mm", tok), g.bcast(p + "b2_b", g.param(p + "b2", [H]), tok)], tok)
+        r2 = g.ew(p + "r2", "add", [f2, ln1], tok)
+        x = _layernorm(g, r2, [T], H, p + "ln2_", g.param(p + "g2", [H]), g.param(p + "be2", [H]))
+    outs.append(x)
+    dy = g.param("dy_top", tok)
+    for l in reversed(range(layers)):
+        p = "b%d_" % l
+        dr2, dg2, dbe2 = _layernorm_bwd(g, dy, g.param(p + "r2", tok), [T], H, p + "ln2_", g.param(p + "g2", [H]))
+        db2 = g.reduce(p + "db2", dr2, [0], [H])
+        ff = [T, I]
+        df1 = _gelu_bwd(g, g.param(p + "dg_mm", ff), g.param(p + "f1", ff), ff, p + "gl_")
+        db1 = g.reduce(p + "db1", df1, [0], [I])
+        dln1 = g.ew(p + "dln1", "add", [g.param(p + "dln1_mm", tok), dr2], tok)
+        dr1, dg1, dbe1 = _layernorm_bwd(g, dln1, g.param(p + "r1", tok), [T], H, p + "ln1_", g.param(p + "g1", [H]))
+        dbo = g.reduce(p + "dbo", dr1, [0], [H])
+        sc = [RA, seq]
+        pr = g.param(p + "probs", sc)
+        t = g.ew(p + "sm_t", "multiply", [g.param(p + "dp_mm", sc), pr], sc)
+        rs = g.reduce(p + "sm_rs", t, [1], [RA])
+        u = g.ew(p + "sm_u", "subtract", [t, g.ew(p + "sm_prs", "multiply", [pr, g.bcast(p + "sm_rs_b", rs, sc)], sc)], sc)
+        dsc = g.ew(p + "dscores", "multiply", [u, _cbcast(g, p + "sm_scale", 1.0 / math.sqrt(H / heads), sc)], sc)
+        dbqkv = g.reduce(p + "dbqkv", g.param(p + "dqkv_mm", [T, 3 * H]), [0], [3 * H])
+        dy = g.ew(p + "dx", "add", [dr1, g.param(p + "dx_mm", tok)], tok)
+        outs += [dr2, dg2, dbe2, db2, df1, db1, dg1, dbe1, dbo, dsc, dbqkv]
+    outs.append(dy)
+    return g.graph(outs)
+
+
+# bert joins CONFIGS once the planner scales to it (see DESIGN.md "planner").
+
+# Full-size keyword arguments are each builder's defaults (BASELINE.json
+# configs); SMALL are the parity-test sizes the CPU oracle finishes in
+# seconds, with ragged extents where the builder allows them.
+SMALL = {
+    "layernorm": dict(rows=256, cols=768),
+    "softmax": dict(heads=2, seq=128),
+    "encoder": dict(batch=2, seq=64, hidden=1024),
+    "gru": dict(batch=64, n=64),
+    "bert": dict(layers=1, batch=2, seq=32, hidden=64, heads=2, inter=256),
+}
+
+# Per-GPU batch extent of each config (the shard axis) and the keyword that
+# sets it: bench.py runs `batch` per rank (weak scaling).
+BATCH_KW = {"layernorm": "rows", "softmax": "heads", "encoder": "batch", "gru": "batch", "bert": "batch"}
+
+
+def shard_layout(name, **kw):
+    """How config `name` splits along its batch axis (the data-parallel
+    shard axis; no exchange between shards).
+
+    Returns (batch, {tensor id: rows per batch item}) for every graph input
+    and output whose leading extent grows linearly with the batch: rows
+    [lo * r, hi * r) of such a tensor belong to batch items [lo, hi).
+    Tensors not listed (e.g. the column-reduced bias gradient) are per-shard
+    partial reductions over the shard's rows."""
+    fn = CONFIGS.get(name) or {"bert": bert}[name]
+    bk = BATCH_KW[name]
+    import inspect
+    batch = kw.get(bk, inspect.signature(fn).parameters[bk].default)
+    full = fn(**kw)
+    one = {n["id"]: n["shape"]["dims"] for n in fn(**dict(kw, **{bk: 1}))["nodes"]}
+    two = {n["id"]: n["shape"]["dims"] for n in fn(**dict(kw, **{bk: 2}))["nodes"]}
+    rows = {}
+    for n in full["nodes"]:
+        d, i = n["shape"]["dims"], n["id"]
+        if d and one.get(i) and two.get(i) and d[0] == batch * one[i][0] and two[i][0] == 2 * one[i][0]:
+            rows[i] = one[i][0]
+    return batch, rows
+
+
+def shard_range(batch, world, rank):
+    """Batch items [lo, hi) of `rank` out of `world` (balanced, contiguous)."""
+    base, extra = divmod(batch, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)

@@ -1,0 +1,48 @@
+"""Shared test helpers (random DAG generator, GPU run helper)."""
+import random
+
+import numpy as np
+
+ELEM_BIN = ["add", "subtract", "multiply", "divide", "maximum", "minimum"]
+ELEM_UN = ["exp", "negate", "log", "rsqrt"]
+
+
+def random_dag(seed, n_ops=12, dims=(64, 256), reduce_p=0.2):
+    """Seeded random graph in the reference JSON format over one 2-D shape:
+    elementwise ops, row / column reductions and broadcasts back."""
+    rng = random.Random(seed)
+    R, C = dims
+    nodes = [{"id": "p0", "kind": "parameter", "shape": {"dims": [R, C], "dtype": "f32"}},
+             {"id": "p1", "kind": "parameter", "shape": {"dims": [R, C], "dtype": "f32"}}]
+    full = ["p0", "p1"]
+    for i in range(n_ops):
+        nid = "n%02d" % i
+        r = rng.random()
+        if r < reduce_p:
+            src = rng.choice(full)
+            if rng.random() < 0.5:
+                nodes.append({"id": nid + "r", "kind": "reduce", "operands": [src], "reduce_dims": [1],
+                              "shape": {"dims": [R], "dtype": "f32"}})
+            else:
+                nodes.append({"id": nid + "r", "kind": "reduce", "operands": [src], "reduce_dims": [0],
+                              "shape": {"dims": [C], "dtype": "f32"}})
+            nodes.append({"id": nid, "kind": "elementwise", "name": "broadcast", "operands": [nid + "r"],
+                          "shape": {"dims": [R, C], "dtype": "f32"}})
+        elif r < 0.4:
+            nodes.append({"id": nid, "kind": "elementwise", "name": rng.choice(["exp", "negate"]),
+                          "operands": [rng.choice(full)], "shape": {"dims": [R, C], "dtype": "f32"}})
+        else:
+            a, b = rng.choice(full), rng.choice(full)
+            nodes.append({"id": nid, "kind": "elementwise", "name": rng.choice(["add", "subtract", "multiply"]),
+                          "operands": [a, b], "shape": {"dims": [R, C], "dtype": "f32"}})
+        full.append(nid)
+    consumed = {o for n in nodes for o in n.get("operands", [])}
+    outs = [n["id"] for n in nodes if n["id"] not in consumed and n["kind"] != "parameter"]
+    if not outs:
+        outs = [full[-1]]
+    return {"nodes": nodes, "outputs": outs}
+
+
+def scaled_inputs(graph, seed=0, scale=0.5):
+    from oracle import executor as orc
+    return orc.random_inputs(graph, seed=seed, scale=scale)

@@ -1,0 +1,165 @@
+"""GPU parity: stitched sm_100a kernels (through the C ABI) against the CPU
+oracle at the stated tolerance (oracle/tolerance.py):
+|got - ref| <= max(1e-5 |ref|, 1e-6) + 2 * (fp32 forward error bound, with the
+worst-case (n-1)u sum|x| reduction-order term).
+
+Covers every config at parity sizes under both shared limits, the unfused
+one-kernel-per-op baseline, the SECTIONED fallback, ragged extents, full
+BASELINE sizes (row-sampled through the shard layout), the host-buffer path,
+CUDA-graph replay and run-to-run determinism."""
+import numpy as np
+import pytest
+
+from oracle import executor as orc
+from oracle import tolerance
+from paper_1911_11576_b200 import runtime as rt
+from paper_1911_11576_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    torch.cuda.set_device(0)
+
+
+def run_device(fused, ins, **kw):
+    ex = rt.Executor(fused, device=0, **kw)
+    d_in = [torch.from_numpy(np.ascontiguousarray(ins[i])).cuda() for i in ex.input_ids]
+    d_out = [torch.full(t["dims"], float("nan"), dtype=torch.float32, device="cuda") for t in ex.info["outputs"]]
+    s = torch.cuda.current_stream().cuda_stream
+    ex.run(d_in, d_out, stream=s)
+    torch.cuda.synchronize()
+    return ex, [o.cpu().numpy() for o in d_out]
+
+
+def assert_parity(g, fused, ins, **kw):
+    ex, got = run_device(fused, ins, **kw)
+    ref, bound = tolerance.reference_with_bound(g, ins)
+    # executor outputs follow the fused graph's output order == the source graph's
+    assert len(got) == len(ref)
+    for k, (a, r, b) in enumerate(zip(got, ref, bound)):
+        ok, worst = tolerance.check(a, r, b)
+        assert ok, "output %d: worst err/tol %.3g" % (k, worst)
+    return ex
+
+
+@pytest.mark.parametrize("name", list(W.CONFIGS))
+@pytest.mark.parametrize("lim", ["b200", "ref48k", "unfused"])
+def test_small_parity(name, lim):
+    g = W.CONFIGS[name](**W.SMALL[name])
+    fused = g if lim == "unfused" else rt.plan(
+        g, shared_limit_bytes=W.B200_SHARED_LIMIT if lim == "b200" else W.REFERENCE_SHARED_LIMIT)["fused"]
+    assert_parity(g, fused, orc.random_inputs(g, seed=11))
+
+
+@pytest.mark.parametrize("name", list(W.CONFIGS))
+def test_sectioned_fallback_parity(name):
+    g = W.CONFIGS[name](**W.SMALL[name])
+    fused = rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT)["fused"]
+    ex = assert_parity(g, fused, orc.random_inputs(g, seed=12), allow_row=False)
+    assert all(k["scheme"] in ("sectioned", "flat") for k in ex.info["kernels"])
+
+
+RAGGED = [
+    ("layernorm", dict(rows=1, cols=768)),
+    ("layernorm", dict(rows=37, cols=770)),
+    ("layernorm", dict(rows=64, cols=33)),
+    ("layernorm", dict(rows=5, cols=4096)),
+    ("layernorm", dict(rows=3, cols=12288)),
+    ("softmax", dict(heads=3, seq=100)),
+    ("softmax", dict(heads=1, seq=1024)),
+    ("encoder", dict(batch=1, seq=7, hidden=96)),
+    ("encoder", dict(batch=3, seq=5, hidden=1000)),
+    ("gru", dict(batch=5, n=16)),
+    ("gru", dict(batch=7, n=50)),
+    ("gru", dict(batch=2, n=128)),
+]
+
+
+@pytest.mark.parametrize("name,kw", RAGGED, ids=["%s-%s" % (n, "-".join(map(str, k.values()))) for n, k in RAGGED])
+def test_ragged_parity(name, kw):
+    g = W.CONFIGS[name](**kw)
+    ins = orc.random_inputs(g, seed=13)
+    for lim in (W.B200_SHARED_LIMIT, W.REFERENCE_SHARED_LIMIT):
+        assert_parity(g, rt.plan(g, shared_limit_bytes=lim)["fused"], ins)
+    assert_parity(g, g, ins)
+
+
+@pytest.mark.parametrize("name", list(W.CONFIGS))
+def test_full_size_row_sampled(name):
+    """Full BASELINE size on the GPU; batch items [0, 2) and the last two
+    are checked against the oracle on those items (every config is
+    independent per batch item); per-shard column reductions (encoder's
+    dbias) against an fp64 reduction of the full input."""
+    g = W.CONFIGS[name]()
+    batch, rows = W.shard_layout(name)
+    fused = rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT)["fused"]
+    rng = np.random.default_rng(21)
+    nodes = {n["id"]: n for n in g["nodes"]}
+    ins = {i: rng.standard_normal(nodes[i]["shape"]["dims"], dtype=np.float32) for i in orc.graph_inputs(g)}
+    ex, got = run_device(fused, ins)
+    outs = orc.graph_outputs(g)
+    bk = W.BATCH_KW[name]
+    for lo, hi in ((0, 2), (batch - 2, batch)):
+        sg = W.CONFIGS[name](**{bk: hi - lo})
+        sin = {i: (v[lo * rows[i]:hi * rows[i]] if i in rows else v) for i, v in ins.items()}
+        ref, bound = tolerance.reference_with_bound(sg, sin)
+        for o, a, r, b in zip(outs, got, ref, bound):
+            if o not in rows:
+                continue
+            ok, worst = tolerance.check(a[lo * rows[o]:hi * rows[o]], r, b)
+            assert ok, "%s rows %d:%d worst %.3g" % (o, lo, hi, worst)
+    for o, a in zip(outs, got):
+        if o in rows:
+            continue
+        node = nodes[o]
+        assert node["kind"] == "reduce"
+        x = ins[node["operands"][0]].astype(np.float64)
+        r = x.sum(axis=tuple(node["reduce_dims"]))
+        n = int(np.prod([x.shape[d] for d in node["reduce_dims"]]))
+        b = (n - 1) * tolerance.U * np.abs(x).sum(axis=tuple(node["reduce_dims"]))
+        ok, worst = tolerance.check(a, r, b)
+        assert ok, worst
+
+
+def test_host_path_graph_replay_and_determinism():
+    g = W.encoder(**W.SMALL["encoder"])
+    fused = rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT)["fused"]
+    ins = orc.random_inputs(g, seed=31)
+    ex, first = run_device(fused, ins)
+    # CUDA-graph replay (same pointers) and a second executor: bit-identical
+    d_in = [torch.from_numpy(ins[i]).cuda() for i in ex.input_ids]
+    d_out = [torch.empty(t["dims"], dtype=torch.float32, device="cuda") for t in ex.info["outputs"]]
+    s = torch.cuda.Stream()
+    for _ in range(3):
+        ex.run(d_in, d_out, stream=s.cuda_stream)
+    torch.cuda.synchronize()
+    for a, b in zip(first, d_out):
+        assert np.array_equal(a, b.cpu().numpy())
+    # host buffers through stitch_executor_run_host
+    h_in = [torch.from_numpy(ins[i]).pin_memory() for i in ex.input_ids]
+    h_out = [torch.empty(t["dims"], dtype=torch.float32).pin_memory() for t in ex.info["outputs"]]
+    ex.run_host(h_in, h_out, stream=s.cuda_stream)
+    for a, b in zip(first, h_out):
+        assert np.array_equal(a, b.numpy())
+    # direct launches (no graph) agree too
+    ex2, second = run_device(fused, ins, use_graph=False)
+    for a, b in zip(first, second):
+        assert np.array_equal(a, b)
+
+
+def test_profile_reports_every_kernel():
+    g = W.softmax(**W.SMALL["softmax"])
+    fused = rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT)["fused"]
+    ins = orc.random_inputs(g, seed=41)
+    ex, _ = run_device(fused, ins)
+    d_in = [torch.from_numpy(ins[i]).cuda() for i in ex.input_ids]
+    d_out = [torch.empty(t["dims"], dtype=torch.float32, device="cuda") for t in ex.info["outputs"]]
+    prof = ex.profile(d_in, d_out, stream=torch.cuda.current_stream().cuda_stream, iters=3)
+    assert [k["name"] for k in prof["kernels"]] == [k["name"] for k in ex.info["kernels"]]
+    assert all(k["us"] > 0 for k in prof["kernels"])

@@ -1,0 +1,158 @@
+"""Fusion-plan parity: the product planner (libstitch_b200.so, C ABI
+stitch_debug_call / stitch_plan_graph) against the REFERENCE planner compiled
+from its own sources (oracle/_ref, reference proj/src/*.cpp). Every stage is
+compared on identical arguments, bit for bit (scores as IEEE doubles).
+
+Reference functions exercised (file:line in /root/reference/proj/src):
+  topological_sort graph.cpp, contract_plan graph.cpp, substitution_fusion /
+  multi_step_patterns / exploratory_fusion / select_seeds pattern_gen.cpp,
+  saved_bytes / m_of_v / score_model_based / shared_feasible cost_model.cpp,
+  canonical_shared_requests / shared_planning / PostDominance emitter.cpp,
+  solve / solve_with_cycle_elimination ilp_solver.cpp, apply_plan
+  transform.cpp, run_plan pipeline.cpp.
+"""
+import json
+import random
+
+import pytest
+
+from conftest import strip_plan
+from helpers import random_dag
+from paper_1911_11576_b200 import runtime as rt
+from paper_1911_11576_b200 import workloads as W
+
+FIXTURES = ["fig1", "thread", "warp", "block", "packing", "all_partition"]
+
+
+def fixture_graph(name):
+    with open("/root/reference/proj/fixtures/%s.json" % name) as f:
+        return json.load(f)
+
+
+def both(ref, fn, **args):
+    return rt.debug_call(fn, **args), ref.call(fn, **args)
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+@pytest.mark.parametrize("lim", [W.REFERENCE_SHARED_LIMIT, W.B200_SHARED_LIMIT])
+def test_fixture_plans(ref, name, lim):
+    g = fixture_graph(name)
+    a, b = both(ref, "plan", graph=g, shared_limit_bytes=lim)
+    assert strip_plan(a) == strip_plan(b)
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+def test_fixture_stages(ref, name):
+    g = fixture_graph(name)
+    for fn in ("topo", "seeds", "multi_step", "generate_patterns"):
+        a, b = both(ref, fn, graph=g)
+        assert a == b, fn
+    pats = rt.debug_call("generate_patterns", graph=g)
+    for p in pats:
+        a, b = both(ref, "pattern_info", graph=g, nodes=p["nodes"])
+        assert a == b, p["nodes"]
+        a, b = both(ref, "postdom", graph=g, nodes=p["nodes"])
+        assert sorted(map(tuple, a)) == sorted(map(tuple, b))
+
+
+@pytest.mark.parametrize("name", list(W.CONFIGS))
+@pytest.mark.parametrize("lim", [W.REFERENCE_SHARED_LIMIT, W.B200_SHARED_LIMIT])
+def test_workload_plans_small(ref, name, lim):
+    g = W.CONFIGS[name](**W.SMALL[name])
+    a, b = both(ref, "plan", graph=g, shared_limit_bytes=lim)
+    assert strip_plan(a) == strip_plan(b)
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_random_dag_plans(ref, seed):
+    g = random_dag(seed, n_ops=6 + seed % 9, dims=(64 + 64 * (seed % 5), 256 * (1 + seed % 4)))
+    for fn in ("topo", "multi_step", "generate_patterns"):
+        a, b = both(ref, fn, graph=g)
+        assert a == b, fn
+    a, b = both(ref, "plan", graph=g, shared_limit_bytes=[W.REFERENCE_SHARED_LIMIT, W.B200_SHARED_LIMIT][seed % 2])
+    assert strip_plan(a) == strip_plan(b)
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_random_substitution_and_contract(ref, seed):
+    rng = random.Random(seed)
+    g = random_dag(seed, n_ops=10)
+    ids = [n["id"] for n in g["nodes"] if n["kind"] != "parameter"]
+    parts = rng.sample(ids, rng.randint(0, len(ids)))
+    a, b = both(ref, "substitution", graph=g, parts=parts)
+    assert a == b
+    # random disjoint plan for contraction
+    pool = ids[:]
+    rng.shuffle(pool)
+    plan = []
+    while pool:
+        k = rng.randint(1, 4)
+        plan.append(pool[:k])
+        pool = pool[k:]
+    a, b = both(ref, "contract", graph=g, plan=plan)
+    assert a == b
+
+
+@pytest.mark.parametrize("seed", range(200))
+def test_ilp_solve_random(ref, seed):
+    """SPEC acceptance 1: random instances (k <= 12), exact optimum equal to
+    the reference and to exhaustive enumeration."""
+    rng = random.Random(seed)
+    k = rng.randint(1, 12)
+    scores = [round(rng.uniform(0, 100), rng.choice([0, 1, 3])) for _ in range(k)]
+    pairs = [[u, v] for u in range(k) for v in range(u + 1, k) if rng.random() < 0.3]
+    cycles = [sorted(rng.sample(range(k), rng.randint(1, min(3, k)))) for _ in range(rng.randint(0, 2))]
+    args = dict(num_vars=k, scores=scores, pairs=pairs, cycles=cycles)
+    a, b = both(ref, "solve", **args)
+    assert a == b
+    best = 0.0
+    for mask in range(1 << k):
+        sel = [i for i in range(k) if mask >> i & 1]
+        if any(mask >> u & 1 and mask >> v & 1 for u, v in pairs):
+            continue
+        if any(sum(mask >> i & 1 for i in c) > len(c) - 1 for c in cycles):
+            continue
+        tot = 0.0
+        for i in sel:
+            tot += scores[i]
+        best = max(best, tot)
+    assert a["total"] == best
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_cycle_elimination_random(ref, seed):
+    """SPEC acceptance 2: adversarial overlapping patterns on random DAGs;
+    same plan as the reference and an acyclic contraction."""
+    rng = random.Random(1000 + seed)
+    g = random_dag(seed, n_ops=8 + seed % 8)
+    ids = [n["id"] for n in g["nodes"] if n["kind"] != "parameter"]
+    pats = [sorted(rng.sample(ids, rng.randint(1, min(5, len(ids))))) for _ in range(rng.randint(2, 9))]
+    scores = [float(rng.randint(1, 50)) for _ in pats]
+    a, b = both(ref, "solve_cycle", graph=g, patterns=pats, scores=scores)
+    assert a == b
+    chosen = [pats[i] for i in a["selected"]]
+    assert "cycle" not in rt.debug_call("contract", graph=g, plan=chosen)
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_shared_planning_random(ref, seed):
+    """SPEC acceptance 5 (safety) + parity of the dominance-tree reuse."""
+    rng = random.Random(seed)
+    g = random_dag(seed, n_ops=10)
+    ids = [n["id"] for n in g["nodes"] if n["kind"] != "parameter"]
+    nodes = sorted(rng.sample(ids, rng.randint(2, len(ids))))
+    reqs = [{"op": i, "bytes": rng.choice([256, 1024, 4096])} for i in nodes if rng.random() < 0.5]
+    a, b = both(ref, "shared_planning", graph=g, nodes=nodes, requests=reqs)
+    assert a == b
+    assert a["total"] <= sum(r["bytes"] for r in reqs)
+
+
+def test_m_of_v_and_scores(ref):
+    vs = [0, 1, 1000, 1 << 20, 3 << 20, 1 << 30, 1 << 40]
+    a, b = both(ref, "m_of_v", v=vs)
+    assert a == b
+    g = fixture_graph("fig1")
+    for per, fused in (([5, 5, 5], 10.0), ([1.0, 2.5], None), ([3, 3, 3], 25.0)):
+        nodes = ["dot_1", "multiply_1", "exp_1"][: len(per)]
+        a, b = both(ref, "score_execution", graph=g, nodes=nodes, per_op_us=per, fused_us=fused)
+        assert a == b
