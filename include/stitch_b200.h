@@ -52,7 +52,8 @@ typedef struct stitch_executor stitch_executor;
  * instead of kernel-sketch text, every fused op of `fused_graph_json`
  * becomes ONE compiled sm_100a kernel composed from the stitched device
  * templates, and every unfused kernel op one plain kernel. options_json:
- * {"device": int, "smem_limit_bytes": int, "cache_dir": str,
+ * {"device": int, "smem_limit_bytes": int, "cache_dir": str, "chunking": bool,
+ *  "chunk_l2_bytes": int, "max_chunks": int,
  *  "use_graph": bool}. The executor owns an HBM arena for intermediates. */
 STITCH_API int stitch_executor_create(const char* fused_graph_json, const char* options_json, stitch_executor** out);
 STITCH_API void stitch_executor_destroy(stitch_executor* ex);

@@ -96,6 +96,8 @@ struct Component {
   std::vector<int64_t> smem_off;  // floats within the row-group slab
   int64_t slab_floats = 0;
   bool tma = false;
+  bool dbuf = false;          // external TMA tiles double-buffered (prefetch the next row)
+  int64_t ext_floats = 0;     // floats of one copy of the external staged tiles
   std::vector<int> cross, post, free_out;
   int64_t max_grid = 1;
 };
@@ -163,6 +165,7 @@ class Builder {
   bool uses_barrier_ = false;
   std::map<int, int64_t> ws_off_;  // value -> workspace offset (floats)
   std::map<int, std::string> cross_parts_;  // cross value -> nparts expression
+  bool chunked_ = false;  // the single ROW component runs rows [row_lo, row_hi) (launch-time chunking)
 };
 
 // ---------------------------------------------------------------------------
@@ -456,20 +459,29 @@ bool Builder::plan_row(Component& c) {
   }
   if (max_inner > static_cast<int64_t>(c.NT) * 64) return false;  // too large for registers
   // shared-memory slab per row group
+  // Slab layout: computed staged values first, then the external (TMA)
+  // tiles; with double buffering a second copy of the external tiles
+  // follows so the next row's loads overlap this row's compute.
   int64_t off = 0;
-  for (int v = 0; v < N; ++v)
-    if (c.staged[v]) {
-      c.smem_off.resize(N, -1);
-      c.smem_off[v] = off;
-      off += (prod(vals_[v].dims, k) + 3) / 4 * 4;
-    }
-  c.smem_off.resize(N, -1);
+  c.smem_off.assign(N, -1);
+  for (int pass = 0; pass < 2; ++pass)
+    for (int v = 0; v < N; ++v)
+      if (c.staged[v] && vals_[v].external == (pass == 1)) {
+        c.smem_off[v] = off;
+        const int64_t f = (prod(vals_[v].dims, k) + 3) / 4 * 4;
+        off += f;
+        if (pass == 1) c.ext_floats += f;
+      }
   c.slab_floats = off;
   if (c.cta) {
     bool tma_ok = true;
     for (int v = 0; v < N; ++v)
       if (c.staged[v] && vals_[v].external) tma_ok = tma_ok && prod(vals_[v].dims, k) % 4 == 0;
     c.tma = tma_ok && std::any_of(inputs_.begin(), inputs_.end(), [&](int v) { return c.staged[v] != 0; });
+    if (c.tma && (c.slab_floats + c.ext_floats + 32 + 8) * 4 <= opts_.max_smem) {
+      c.dbuf = true;
+      c.slab_floats += c.ext_floats;
+    }
   }
   const int64_t slab_bytes = (c.slab_floats + 32) * 4;
   if (c.cta ? slab_bytes > opts_.max_smem : slab_bytes * 8 > opts_.max_smem) return false;
@@ -662,6 +674,8 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
   (void)cta_rank;
   open("");
   ln("// row scheme: k=" + std::to_string(k) + " rows=" + std::to_string(c.R) + " threads/row=" + std::to_string(NT));
+  const std::string rlo = chunked_ ? "row_lo" : "0LL";
+  const std::string rhi = chunked_ ? "row_hi" : std::to_string(c.R) + "LL";
   if (c.cta) {
     ln("const int t = threadIdx.x;");
     ln("float* slab = smem;");
@@ -675,7 +689,8 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
   ln("float* red = slab + " + std::to_string(c.slab_floats) + ";");
   ln("(void)red;");
   for (int v = 0; v < static_cast<int>(vals_.size()); ++v)
-    if (c.staged[v]) ln("float* sm" + std::to_string(v) + " = slab + " + std::to_string(c.smem_off[v]) + ";  // " + vals_[v].id);
+    if (c.staged[v] && !(c.dbuf && vals_[v].external))
+      ln("float* sm" + std::to_string(v) + " = slab + " + std::to_string(c.smem_off[v]) + ";  // " + vals_[v].id);
 
   // Free outputs (not depending on rows): grid-stride over their elements.
   for (int f : c.free_out) {
@@ -705,13 +720,33 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
     }
   }
 
+  // External tiles of one row: total bytes and the bulk copies into buffer `b`.
+  int64_t tma_bytes = 0;
+  for (int v : inputs_)
+    if (c.staged[v]) tma_bytes += prod(vals_[v].dims, k) * 4;
+  auto issue_tma = [&](const std::string& r, const std::string& b) {
+    ln("stitch_dev::mbar_expect_tx(bar + " + b + ", " + std::to_string(tma_bytes) + "u);");
+    for (int v : inputs_)
+      if (c.staged[v]) {
+        const int64_t S = prod(vals_[v].dims, k);
+        ln("stitch_dev::bulk_g2s(slab + " + std::to_string(c.smem_off[v]) + " + " + b + " * " + std::to_string(c.ext_floats) +
+           ", " + in_ptr(v) + " + (" + r + ") * " + std::to_string(S) + "LL, " + std::to_string(S * 4) + "u, bar + " + b + ");");
+      }
+  };
   if (c.tma) {
     ln("stitch_dev::u64* bar = reinterpret_cast<stitch_dev::u64*>(smem + " + std::to_string(c.slab_floats + 32) + ");");
-    ln("if (t == 0) stitch_dev::mbar_init(bar, 1);");
+    ln(c.dbuf ? "if (t == 0) { stitch_dev::mbar_init(bar, 1); stitch_dev::mbar_init(bar + 1, 1); }"
+              : "if (t == 0) stitch_dev::mbar_init(bar, 1);");
     ln("__syncthreads();");
     ln("unsigned phase = 0;");
+    if (c.dbuf) {
+      ln("int buf = 0;");
+      open("if (t == 0 && " + rlo + " + g0 < " + rhi + ")");
+      issue_tma(rlo + " + g0", "0");
+      close();
+    }
   }
-  open("for (long long row = g0; row < " + std::to_string(c.R) + "LL; row += gstride)");
+  open("for (long long row = " + rlo + " + g0; row < " + rhi + "; row += gstride" + (c.dbuf ? ", buf ^= 1" : "") + ")");
   reg_.clear();
   scalar_.clear();
   memo_.emplace_back();
@@ -722,18 +757,21 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
   for (int v : inputs_)
     if (c.staged[v]) any_ext_staged = true;
   if (any_ext_staged) {
-    if (c.tma) {
-      int64_t bytes = 0;
+    if (c.dbuf) {
+      // prefetch the next row into the other buffer (its readers finished at
+      // the previous iteration's trailing barrier), then wait for this one
+      open("if (t == 0 && row + gstride < " + rhi + ")");
+      issue_tma("row + gstride", "(buf ^ 1)");
+      close();
+      ln("stitch_dev::mbar_wait(bar + buf, (phase >> buf) & 1u);");
+      ln("phase ^= 1u << buf;");
       for (int v : inputs_)
-        if (c.staged[v]) bytes += prod(vals_[v].dims, k) * 4;
+        if (c.staged[v])
+          ln("float* sm" + std::to_string(v) + " = slab + " + std::to_string(c.smem_off[v]) + " + buf * " +
+             std::to_string(c.ext_floats) + ";  // " + vals_[v].id);
+    } else if (c.tma) {
       open("if (t == 0)");
-      ln("stitch_dev::mbar_expect_tx(bar, " + std::to_string(bytes) + "u);");
-      for (int v : inputs_)
-        if (c.staged[v]) {
-          const int64_t S = prod(vals_[v].dims, k);
-          ln("stitch_dev::bulk_g2s(sm" + std::to_string(v) + ", " + in_ptr(v) + " + row * " + std::to_string(S) +
-             "LL, " + std::to_string(S * 4) + "u, bar);");
-        }
+      issue_tma("row", "0");
       close();
       ln("stitch_dev::mbar_wait(bar, phase);");
       ln("phase ^= 1u;");
@@ -905,9 +943,42 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
                                     : vals_[b].dims;
       const int64_t Nn = od.back();
       const bool fast = op.type == OpType::kBatchedDot && L.vec == 4 && Nn % 4 == 0 && !L.guard;
+      // Register tile: the L.iters row chunks a thread owns share its
+      // column quad, so each k step loads one B quad and one A quad per
+      // owned row (k-vectorised) and issues 16 FMAs per B quad.
+      const bool tiled = fast && od.size() == 2 && (static_cast<int64_t>(NT) * 4) % Nn == 0 && K % 4 == 0 &&
+                         c.staged[a] && c.staged[b];
       std::string r = "r" + std::to_string(m);
       ln("float " + r + "[" + std::to_string(L.elems()) + "];  // " + vals_[m].id + " (gemm stage)");
-      if (fast) {
+      if (tiled) {
+        const int64_t RS = static_cast<int64_t>(NT) * 4 / Nn;  // rows between a thread's row chunks
+        const int I = L.iters;
+        open("");
+        ln("const int n0 = (4 * t) % " + std::to_string(Nn) + ", m0 = (4 * t) / " + std::to_string(Nn) + ";");
+        ln("const float* A = sm" + std::to_string(a) + " + m0 * " + std::to_string(K) + ";");
+        ln("const float* B = sm" + std::to_string(b) + " + n0;");
+        ln("float acc[" + std::to_string(I * 4) + "];");
+        ln("#pragma unroll");
+        ln("for (int e = 0; e < " + std::to_string(I * 4) + "; ++e) acc[e] = 0.f;");
+        ln("#pragma unroll 2");
+        open("for (int kk = 0; kk < " + std::to_string(K) + "; kk += 4)");
+        ln("float4 av[" + std::to_string(I) + "];");
+        ln("#pragma unroll");
+        ln("for (int i = 0; i < " + std::to_string(I) + "; ++i) av[i] = *reinterpret_cast<const float4*>(A + i * " +
+           std::to_string(RS * K) + " + kk);");
+        for (int j = 0; j < 4; ++j) {
+          const char* comp = j == 0 ? "x" : j == 1 ? "y" : j == 2 ? "z" : "w";
+          ln("{ const float4 bv = *reinterpret_cast<const float4*>(B + (kk + " + std::to_string(j) + ") * " + std::to_string(Nn) + ");");
+          ln("#pragma unroll");
+          ln("  for (int i = 0; i < " + std::to_string(I) + "; ++i) { const float s = av[i]." + comp +
+             "; acc[i * 4 + 0] = fmaf(s, bv.x, acc[i * 4 + 0]); acc[i * 4 + 1] = fmaf(s, bv.y, acc[i * 4 + 1]); "
+             "acc[i * 4 + 2] = fmaf(s, bv.z, acc[i * 4 + 2]); acc[i * 4 + 3] = fmaf(s, bv.w, acc[i * 4 + 3]); } }");
+        }
+        close();
+        ln("#pragma unroll");
+        ln("for (int e = 0; e < " + std::to_string(I * 4) + "; ++e) " + r + "[e] = acc[e];");
+        close();
+      } else if (fast) {
         // Output element chunk (.., m, n0..n0+3) per (it): A scalar x B float4.
         const int rb = static_cast<int>(od.size());
         ln("#pragma unroll");
@@ -1106,10 +1177,39 @@ void Builder::emit_row_finalize(std::vector<Component*>& comps) {
       bool scalar = static_cast<int>(op.reduce_dims.size()) == static_cast<int>(vals_[in].dims.size());
       const int64_t So = scalar ? 1 : prod(vals_[in].dims, c->k);
       const std::string Op = op.elem_name == "max" ? "stitch_dev::MaxOp" : "stitch_dev::SumOp";
-      open("for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < " + std::to_string(So) + "LL; i += (long long)gridDim.x * blockDim.x)");
-      ln("const float v = stitch_dev::combine_parts<" + Op + ">(ws + " + std::to_string(ws_off_[x]) + "LL, " + cross_parts_[x] + ", " + std::to_string(So) + "LL, i);");
+      // Parallel fixed-order combine: a CTA owns a block of CW columns, its
+      // threads split the partial rows (slice s of S), then slice 0 joins
+      // the S slice sums in order through shared memory.
+      const int CW = So >= 32 ? 32 : 1;
+      open("");
+      ln("const int CW = " + std::to_string(CW) + ", S = blockDim.x / CW;");
+      ln("const int c = threadIdx.x % CW, s = threadIdx.x / CW;");
+      open("for (long long cb = blockIdx.x; cb * CW < " + std::to_string(So) + "LL; cb += gridDim.x)");
+      ln("const long long i = cb * CW + c;");
+      ln("float a = " + Op + "::init();");
+      ln("if (i < " + std::to_string(So) + "LL) a = stitch_dev::combine_strided<" + Op + ">(ws + " +
+         std::to_string(ws_off_[x]) + "LL, " + cross_parts_[x] + ", " + std::to_string(So) + "LL, i, s, S);");
+      ln("__syncthreads();");
+      ln("smem[s * CW + c] = a;");
+      ln("__syncthreads();");
+      if (CW == 1) {
+        // scalar: warp 0 folds the slices (lane l: slices l, l+32, ...) and
+        // finishes with a fixed xor-shuffle tree
+        open("if (threadIdx.x < 32)");
+        ln("float v = " + Op + "::init();");
+        ln("for (int j = threadIdx.x; j < S; j += 32) v = " + Op + "::apply(v, smem[j]);");
+        ln("v = stitch_dev::warp_allreduce<" + Op + ">(v);");
+        open("if (threadIdx.x == 0)");
+      } else {
+        open("if (s == 0 && i < " + std::to_string(So) + "LL)");
+        ln("float v = " + Op + "::init();");
+        ln("for (int j = 0; j < S; ++j) v = " + Op + "::apply(v, smem[j * CW + c]);");
+      }
       if (vals_[x].output) ln(out_ptr(x) + "[i] = v;");
       if (materialized_.count(x) && !vals_[x].output) ln(materialized_[x] + "[i] = v;");
+      close();
+      if (CW == 1) close();
+      close();
       close();
     }
   bool any_post = false;
@@ -1314,6 +1414,13 @@ KernelSpec Builder::build() {
     }
     std::vector<Component*> rowc;
     std::string scheme;
+    chunked_ = comps.size() == 1 && comps[0].scheme == "row" && comps[0].cross.empty() && comps[0].post.empty() &&
+               comps[0].free_out.empty();
+    if (chunked_) {
+      spec_.chunkable = true;
+      spec_.rows = comps[0].R;
+      spec_.rows_per_cta = comps[0].cta ? 1 : block / 32;
+    }
     for (size_t i = 0; i < comps.size(); ++i) {
       Component& c = comps[i];
       for (int x : c.cross) cross_parts_[x] = "(int)" + n[i];
@@ -1322,7 +1429,7 @@ KernelSpec Builder::build() {
       if (c.scheme == "row") {
         emit_row(c, lo[i], n[i], "");
         rowc.push_back(&c);
-        smem_floats = std::max(smem_floats, c.cta ? c.slab_floats + 32 + 4 : (c.slab_floats + 32) * (block / 32));
+        smem_floats = std::max(smem_floats, c.cta ? c.slab_floats + 32 + 8 : (c.slab_floats + 32) * (block / 32));
         if (!c.cta)
           for (int x : c.cross) {
             const int in = vals_[x].operands[0];
@@ -1335,7 +1442,7 @@ KernelSpec Builder::build() {
         if (has_block) spec_.composition.insert("block");
         std::ostringstream s;
         s << (c.cta ? "row_cta" : "row_warp") << "(k=" << c.k << ",rows=" << c.R << ",nt=" << c.NT
-          << (c.tma ? ",tma" : "") << (c.cross.empty() ? "" : ",cross") << ")";
+          << (c.tma ? (c.dbuf ? ",tma2" : ",tma") : "") << (c.cross.empty() ? "" : ",cross") << ")";
         scheme += (scheme.empty() ? "" : "+") + s.str();
         spec_.max_grid = std::max<int>(spec_.max_grid, static_cast<int>(std::min<int64_t>(c.max_grid, 1 << 20)));
       } else {
@@ -1347,6 +1454,8 @@ KernelSpec Builder::build() {
       memo_.pop_back();
       if (comps.size() > 1) close();
     }
+    for (Component* c : rowc)
+      if (!c->cross.empty()) smem_floats = std::max<int64_t>(smem_floats, block);
     memo_.emplace_back();
     emit_row_finalize(rowc);
     memo_.pop_back();
@@ -1369,6 +1478,8 @@ KernelSpec Builder::build() {
   }
   params.push_back("float* __restrict__ ws");
   params.push_back("unsigned int* __restrict__ gsync");
+  params.push_back("const long long row_lo");
+  params.push_back("const long long row_hi");
   head << "// stitched kernel for fused op '" << name_ << "': " << topo_members_.size() << " ops, scheme "
        << spec_.scheme << "\n";
   for (int m : topo_members_) {
@@ -1381,7 +1492,7 @@ KernelSpec Builder::build() {
   head << "extern \"C\" __global__ void __launch_bounds__(" << block << ") " << name_ << "(" << join(params, ", ")
        << ") {\n";
   head << "  extern __shared__ __align__(128) float smem[];\n";
-  head << "  (void)ws; (void)gsync; (void)smem;\n";
+  head << "  (void)ws; (void)gsync; (void)smem; (void)row_lo; (void)row_hi;\n";
   spec_.source = head.str() + body_src + "}\n";
   spec_.block = block;
   spec_.smem_bytes = static_cast<int>(smem_floats * 4 + (smem_floats ? 16 : 0));

@@ -45,6 +45,12 @@ struct KernelSpec {
   std::vector<std::string> outputs;  // pointer arguments, in order
   int64_t algo_bytes = 0;            // each input read once + each output written once
   int64_t flops = 0;                 // 2*M*N*K summed over gemm stages
+  // Row-chunkable: one ROW component with no cross-row reduction, so the
+  // kernel can run any row range [row_lo, row_hi) (trailing kernel args) and
+  // touches exactly that range's bytes of every rowed tensor.
+  bool chunkable = false;
+  int64_t rows = 0;
+  int rows_per_cta = 1;
 };
 
 struct CodegenOptions {

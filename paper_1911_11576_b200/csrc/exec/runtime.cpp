@@ -116,6 +116,7 @@ Executor::Executor(const Graph& fused, const ExecOptions& opts) : g_(fused), opt
     output_bytes_.push_back(g_.at(o).shape.byte_count());
   }
   build_kernels();
+  plan_chunks();
   plan_arena();
   if (!opts_.compile_only) init_device();
 }
@@ -260,11 +261,59 @@ void Executor::build_kernels() {
   }
 }
 
+void Executor::plan_chunks() {
+  segments_.clear();
+  const int nk = static_cast<int>(kernels_.size());
+  int i = 0;
+  while (i < nk) {
+    Segment seg;
+    seg.first = i;
+    int j = i;
+    if (opts_.chunking && kernels_[i].spec.chunkable)
+      while (j + 1 < nk && kernels_[j + 1].spec.chunkable) ++j;
+    seg.last = j;
+    i = j + 1;
+    // Intermediates produced and fully consumed inside the segment.
+    std::vector<int> local;
+    int64_t inter = 0;
+    for (size_t b = 0; b < bufs_.size(); ++b) {
+      const ValueBuf& x = bufs_[b];
+      if (x.kind == ValueBuf::kArena && x.first >= seg.first && x.last <= seg.last && x.last > x.first) {
+        local.push_back(static_cast<int>(b));
+        inter += x.bytes;
+      }
+    }
+    if (seg.last > seg.first && !local.empty()) {
+      // Smallest power-of-two chunk count that brings the per-chunk
+      // intermediates under the L2 budget, dividing every kernel's rows and
+      // every local buffer, with enough rows per chunk to fill the GPU.
+      int best = 1;
+      for (int C = 2; C <= opts_.max_chunks; C *= 2) {
+        bool ok = true;
+        for (int k = seg.first; k <= seg.last && ok; ++k) {
+          const KernelSpec& sp = kernels_[k].spec;
+          ok = sp.rows % C == 0 && (!opts_.chunk_fill || sp.rows / C >= static_cast<int64_t>(sms_) * 2 * sp.rows_per_cta);
+        }
+        for (int b : local) ok = ok && bufs_[b].bytes % (static_cast<int64_t>(C) * 256) == 0;
+        if (!ok) break;
+        best = C;
+        if (inter / C <= opts_.chunk_l2_bytes) break;
+      }
+      seg.chunks = best;
+      if (best > 1)
+        for (int b : local) bufs_[b].chunks = best;
+    }
+    segments_.push_back(seg);
+  }
+  launches_per_run_ = 0;
+  for (const Segment& sg : segments_) launches_per_run_ += (sg.last - sg.first + 1) * sg.chunks;
+}
+
 void Executor::plan_arena() {
   std::vector<int> order;
   for (size_t b = 0; b < bufs_.size(); ++b)
     if (bufs_[b].kind == ValueBuf::kArena) order.push_back(static_cast<int>(b));
-  std::sort(order.begin(), order.end(), [&](int a, int b) { return bufs_[a].bytes > bufs_[b].bytes; });
+  std::sort(order.begin(), order.end(), [&](int a, int b) { return bufs_[a].arena_bytes() > bufs_[b].arena_bytes(); });
   std::vector<int> placed;
   const int64_t align = 256;
   for (int b : order) {
@@ -272,16 +321,16 @@ void Executor::plan_arena() {
     std::vector<std::pair<int64_t, int64_t>> busy;
     for (int p : placed) {
       const ValueBuf& y = bufs_[p];
-      if (y.first <= x.last && x.first <= y.last) busy.push_back({y.offset, y.offset + y.bytes});
+      if (y.first <= x.last && x.first <= y.last) busy.push_back({y.offset, y.offset + y.arena_bytes()});
     }
     std::sort(busy.begin(), busy.end());
     int64_t off = 0;
     for (auto [lo, hi] : busy) {
-      if (off + x.bytes <= lo) break;
+      if (off + x.arena_bytes() <= lo) break;
       off = std::max(off, (hi + align - 1) / align * align);
     }
     x.offset = off;
-    arena_bytes_ = std::max(arena_bytes_, off + x.bytes);
+    arena_bytes_ = std::max(arena_bytes_, off + x.arena_bytes());
     placed.push_back(b);
   }
   for (KernelInst& k : kernels_) {
@@ -343,44 +392,62 @@ void Executor::init_device() {
 
 void Executor::launch_all(const void* const* inputs, void* const* outputs, void* stream, std::vector<void*>* events) {
   CudaApi& cu = CudaApi::get();
-  auto addr = [&](int b) -> CUdeviceptr {
+  // Address of buffer b as seen by chunk c: a chunk-local buffer holds one
+  // chunk, and kernels index rows absolutely, so shift its base back.
+  auto addr = [&](int b, int c) -> CUdeviceptr {
     const ValueBuf& x = bufs_[b];
     if (x.kind == ValueBuf::kInput) return reinterpret_cast<CUdeviceptr>(inputs[x.slot]);
     if (x.kind == ValueBuf::kOutput) return reinterpret_cast<CUdeviceptr>(outputs[x.slot]);
-    return arena_ + x.offset;
+    return arena_ + x.offset - static_cast<CUdeviceptr>(c) * static_cast<CUdeviceptr>(x.arena_bytes() * (x.chunks > 1));
   };
   std::vector<CUdeviceptr> vals;
+  std::vector<long long> rng(2);
   std::vector<void*> args;
-  for (size_t i = 0; i < kernels_.size(); ++i) {
-    KernelInst& k = kernels_[i];
-    vals.clear();
-    for (int b : k.in_bufs) vals.push_back(addr(b));
-    for (int b : k.out_bufs) vals.push_back(addr(b));
-    vals.push_back(ws_ + k.ws_off * 4);
-    vals.push_back(sync_ + k.sync_off * 4);
-    args.clear();
-    for (CUdeviceptr& v : vals) args.push_back(&v);
-    CUlaunchConfig cfg;
-    std::memset(&cfg, 0, sizeof cfg);
-    cfg.gridDimX = k.grid;
-    cfg.gridDimY = cfg.gridDimZ = 1;
-    cfg.blockDimX = k.spec.block;
-    cfg.blockDimY = cfg.blockDimZ = 1;
-    cfg.sharedMemBytes = k.spec.smem_bytes;
-    cfg.hStream = static_cast<CUstream>(stream);
-    CUlaunchAttribute attr[1];
-    if (k.spec.cooperative) {
-      attr[0].id = CU_LAUNCH_ATTRIBUTE_COOPERATIVE;
-      attr[0].value.cooperative = 1;
-      cfg.attrs = attr;
-      cfg.numAttrs = 1;
-    }
-    if (events) cu_check(cu.cuEventRecord(static_cast<CUevent>((*events)[2 * i]), static_cast<CUstream>(stream)), "event");
-    cu_check(cu.cuLaunchKernelEx(&cfg, static_cast<CUfunction>(k.fn), args.data(), nullptr), k.spec.name.c_str());
-    if (events) cu_check(cu.cuEventRecord(static_cast<CUevent>((*events)[2 * i + 1]), static_cast<CUstream>(stream)), "event");
-  }
+  int launch = 0;
+  for (const Segment& sg : segments_)
+    for (int c = 0; c < sg.chunks; ++c)
+      for (int i = sg.first; i <= sg.last; ++i, ++launch) {
+        KernelInst& k = kernels_[i];
+        vals.clear();
+        for (int b : k.in_bufs) vals.push_back(addr(b, c));
+        for (int b : k.out_bufs) vals.push_back(addr(b, c));
+        vals.push_back(ws_ + k.ws_off * 4);
+        vals.push_back(sync_ + k.sync_off * 4);
+        const int64_t rows = k.spec.chunkable ? k.spec.rows / sg.chunks : 0;
+        rng[0] = static_cast<long long>(rows * c);
+        rng[1] = static_cast<long long>(rows * (c + 1));
+        if (!k.spec.chunkable) rng[0] = rng[1] = 0;
+        args.clear();
+        for (CUdeviceptr& v : vals) args.push_back(&v);
+        args.push_back(&rng[0]);
+        args.push_back(&rng[1]);
+        int grid = k.grid;
+        if (sg.chunks > 1) {
+          const int64_t need = (rows + k.spec.rows_per_cta - 1) / k.spec.rows_per_cta;
+          grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(grid, need)));
+        }
+        if (k.spec.chunkable && sg.chunks == 1) rng[1] = k.spec.rows;
+        CUlaunchConfig cfg;
+        std::memset(&cfg, 0, sizeof cfg);
+        cfg.gridDimX = grid;
+        cfg.gridDimY = cfg.gridDimZ = 1;
+        cfg.blockDimX = k.spec.block;
+        cfg.blockDimY = cfg.blockDimZ = 1;
+        cfg.sharedMemBytes = k.spec.smem_bytes;
+        cfg.hStream = static_cast<CUstream>(stream);
+        CUlaunchAttribute attr[1];
+        if (k.spec.cooperative) {
+          attr[0].id = CU_LAUNCH_ATTRIBUTE_COOPERATIVE;
+          attr[0].value.cooperative = 1;
+          cfg.attrs = attr;
+          cfg.numAttrs = 1;
+        }
+        if (events) cu_check(cu.cuEventRecord(static_cast<CUevent>((*events)[2 * launch]), static_cast<CUstream>(stream)), "event");
+        cu_check(cu.cuLaunchKernelEx(&cfg, static_cast<CUfunction>(k.fn), args.data(), nullptr), k.spec.name.c_str());
+        if (events) cu_check(cu.cuEventRecord(static_cast<CUevent>((*events)[2 * launch + 1]), static_cast<CUstream>(stream)), "event");
+      }
   for (auto [slot, b] : output_copies_)
-    cu_check(cu.cuMemcpyDtoDAsync(reinterpret_cast<CUdeviceptr>(outputs[slot]), addr(b), output_bytes_[slot],
+    cu_check(cu.cuMemcpyDtoDAsync(reinterpret_cast<CUdeviceptr>(outputs[slot]), addr(b, 0), output_bytes_[slot],
                                   static_cast<CUstream>(stream)),
              "output copy");
 }
@@ -445,20 +512,24 @@ void Executor::run_host(const void* const* host_inputs, void* const* host_output
 
 json::Value Executor::profile(const void* const* inputs, void* const* outputs, void* stream, int iters) {
   CudaApi& cu = CudaApi::get();
-  std::vector<void*> ev(2 * kernels_.size());
+  std::vector<void*> ev(2 * launches_per_run_);
   for (void*& e : ev) {
     CUevent x;
     cu_check(cu.cuEventCreate(&x, CU_EVENT_DEFAULT), "event create");
     e = x;
   }
   std::vector<double> acc(kernels_.size(), 0.0);
+  std::vector<int> kernel_of;
+  for (const Segment& sg : segments_)
+    for (int c = 0; c < sg.chunks; ++c)
+      for (int i = sg.first; i <= sg.last; ++i) kernel_of.push_back(i);
   for (int it = 0; it < std::max(1, iters); ++it) {
     launch_all(inputs, outputs, stream, &ev);
     cu_check(cu.cuStreamSynchronize(static_cast<CUstream>(stream)), "sync");
-    for (size_t i = 0; i < kernels_.size(); ++i) {
+    for (int l = 0; l < launches_per_run_; ++l) {
       float ms = 0.f;
-      cu_check(cu.cuEventElapsedTime(&ms, static_cast<CUevent>(ev[2 * i]), static_cast<CUevent>(ev[2 * i + 1])), "elapsed");
-      acc[i] += ms;
+      cu_check(cu.cuEventElapsedTime(&ms, static_cast<CUevent>(ev[2 * l]), static_cast<CUevent>(ev[2 * l + 1])), "elapsed");
+      acc[kernel_of[l]] += ms;
     }
   }
   for (void* e : ev) cu.cuEventDestroy(static_cast<CUevent>(e));
@@ -478,6 +549,7 @@ json::Value Executor::profile(const void* const* inputs, void* const* outputs, v
   }
   out.set("kernels", ks);
   out.set("total_us", total);
+  out.set("launches", launches_per_run_);
   return out;
 }
 
@@ -514,6 +586,8 @@ json::Value Executor::describe() const {
     e.set("cooperative", k.spec.cooperative);
     e.set("algo_bytes", k.spec.algo_bytes);
     e.set("flops", k.spec.flops);
+    e.set("chunkable", k.spec.chunkable);
+    e.set("rows", k.spec.rows);
     e.set("inputs", json::Value::array_of(k.spec.inputs));
     e.set("outputs", json::Value::array_of(k.spec.outputs));
     e.set("cache_hit", k.cache_hit);
@@ -521,6 +595,17 @@ json::Value Executor::describe() const {
     ks.push(e);
   }
   j.set("kernels", ks);
+  json::Value sched = json::Value::array();
+  for (const Segment& sg : segments_) {
+    json::Value e = json::Value::object();
+    json::Value names = json::Value::array();
+    for (int i = sg.first; i <= sg.last; ++i) names.push(kernels_[i].spec.name);
+    e.set("kernels", names);
+    e.set("chunks", sg.chunks);
+    sched.push(e);
+  }
+  j.set("schedule", sched);
+  j.set("launches", launches_per_run_);
   j.set("algo_bytes", algo);
   j.set("arena_bytes", arena_bytes_);
   j.set("workspace_bytes", ws_floats_ * 4);

@@ -24,6 +24,14 @@ struct ExecOptions {
   std::string cache_dir;   // "" = no disk cache
   bool use_graph = true;   // replay launches as a CUDA graph on non-null streams
   bool compile_only = false;  // generate + compile, no device work (build-time cache fill)
+  // L2-resident chunking: consecutive row-chunkable kernels that hand
+  // intermediates to each other run chunk by chunk (rows [c R/C, (c+1) R/C)
+  // of every kernel), each intermediate held in a one-chunk buffer reused by
+  // every chunk, so it stays in L2 and is overwritten before write-back.
+  int64_t chunk_l2_bytes = 24ll << 20;  // target intermediate bytes per chunk (L2 is 126 MB)
+  int max_chunks = 64;
+  bool chunking = true;
+  bool chunk_fill = true;  // require enough rows per chunk to fill every SM (tests force small chunks)
   CodegenOptions codegen;
 };
 
@@ -39,6 +47,12 @@ struct ValueBuf {
   int slot = -1;        // input / output position
   int64_t offset = 0;   // arena byte offset
   int first = -1, last = -1;  // producing / last consuming kernel
+  int chunks = 1;             // > 1: chunk-local intermediate, arena holds bytes / chunks
+  int64_t arena_bytes() const { return bytes / chunks; }
+};
+
+struct Segment {  // kernels [first, last] in launch order, run chunk by chunk when chunks > 1
+  int first = 0, last = 0, chunks = 1;
 };
 
 struct KernelInst {
@@ -73,6 +87,7 @@ class Executor {
   void build_kernels();
   void plan_arena();
   void init_device();
+  void plan_chunks();
   void launch_all(const void* const* inputs, void* const* outputs, void* stream, std::vector<void*>* events);
 
   Graph g_;
@@ -80,6 +95,8 @@ class Executor {
   std::vector<ValueBuf> bufs_;
   std::map<std::string, int> buf_of_;
   std::vector<KernelInst> kernels_;
+  std::vector<Segment> segments_;
+  int launches_per_run_ = 0;
   std::vector<std::string> input_ids_, output_ids_;
   std::vector<int64_t> input_bytes_, output_bytes_;
   std::vector<std::vector<int64_t>> input_dims_, output_dims_;

@@ -163,3 +163,22 @@ def test_profile_reports_every_kernel():
     prof = ex.profile(d_in, d_out, stream=torch.cuda.current_stream().cuda_stream, iters=3)
     assert [k["name"] for k in prof["kernels"]] == [k["name"] for k in ex.info["kernels"]]
     assert all(k["us"] > 0 for k in prof["kernels"])
+
+
+@pytest.mark.parametrize("name", ["softmax", "encoder"])
+def test_chunked_schedule_bit_identical(name):
+    """L2-resident chunked launches (intermediates in one-chunk buffers
+    reused by every chunk) give bit-identical results to whole-tensor
+    launches at the full BASELINE size (parity with the oracle at full size
+    is test_full_size_row_sampled, which runs chunked by default)."""
+    g = W.CONFIGS[name]()
+    fused = rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT)["fused"]
+    rng = np.random.default_rng(51)
+    nodes = {n["id"]: n for n in g["nodes"]}
+    ins = {i: rng.standard_normal(nodes[i]["shape"]["dims"], dtype=np.float32) for i in orc.graph_inputs(g)}
+    ex_c, a = run_device(fused, ins)
+    assert any(s["chunks"] > 1 for s in ex_c.info["schedule"]), ex_c.info["schedule"]
+    ex_n, b = run_device(fused, ins, chunking=False)
+    assert all(s["chunks"] == 1 for s in ex_n.info["schedule"])
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
