@@ -52,6 +52,7 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-unfused", action="store_true")
+    ap.add_argument("--no-model-plan", action="store_true")
     ap.add_argument("--out", default="", help="also write the JSON line to this file")
     return ap.parse_args()
 
@@ -272,6 +273,7 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_1911_11576_b200 import runtime as rt
+    from paper_1911_11576_b200 import tuning
     from paper_1911_11576_b200 import workloads as W
 
     torch.cuda.set_device(local)
@@ -288,16 +290,23 @@ def main():
     for name in names:
         g = W.CONFIGS[name]()
         t0 = time.perf_counter()
-        plan = rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT)
+        plan, plan_kind = tuning.config_plan(name, g)
         plan_ms = (time.perf_counter() - t0) * 1e3
         ex = rt.Executor(plan["fused"], device=local)
-        base = None if args.no_unfused else rt.Executor(g, device=local)
+        model = None
+        if not args.no_model_plan and plan_kind.startswith("execution"):
+            mplan = rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT)
+            model = rt.Executor(mplan["fused"], device=local)
+        base = None if args.no_unfused else rt.Executor(g, device=local, chunking=False)
         ins = [torch.randn(t["dims"], device=dev, generator=gen, dtype=torch.float32) for t in ex.info["inputs"]]
         outs = [torch.empty(t["dims"], device=dev, dtype=torch.float32) for t in ex.info["outputs"]]
         by_id = dict(zip(ex.input_ids, ins))
         ins_b = [by_id[i] for i in base.input_ids] if base else None
         outs_b = [torch.empty(t["dims"], device=dev, dtype=torch.float32) for t in base.info["outputs"]] if base else None
+        ins_m = [by_id[i] for i in model.input_ids] if model else None
+        outs_m = [torch.empty(t["dims"], device=dev, dtype=torch.float32) for t in model.info["outputs"]] if model else None
         cfgs.append(dict(name=name, g=g, ex=ex, base=base, ins=ins, outs=outs, ins_b=ins_b, outs_b=outs_b,
+                         model=model, ins_m=ins_m, outs_m=outs_m, plan_kind=plan_kind,
                          bytes=graph_bytes(g), plan_ms=plan_ms,
                          groups=sum(1 for n in plan["fused"]["nodes"] if n["kind"] == "fused"),
                          kernels=len(ex.info["kernels"])))
@@ -319,6 +328,9 @@ def main():
                 ev_pairs[i][0].record(stream)
                 if which == "fused":
                     c["ex"].run(c["ins"], c["outs"], stream=sh)
+                elif which == "model":
+                    if c["model"]:
+                        c["model"].run(c["ins_m"], c["outs_m"], stream=sh)
                 else:
                     c["base"].run(c["ins_b"], c["outs_b"], stream=sh)
                 ev_pairs[i][1].record(stream)
@@ -357,6 +369,9 @@ def main():
     base_ms = None
     if not args.no_unfused:
         base_ms, _ = measure("unfused", args.steps, max(3, args.warmup))
+    model_ms = None
+    if any(c["model"] for c in cfgs):
+        model_ms, _ = measure("model", args.steps, max(3, args.warmup))
 
     total_bytes = sum(c["bytes"] for c in cfgs)
     step_ms = float(fused_ms.sum())
@@ -385,7 +400,7 @@ def main():
     for i, c in enumerate(cfgs):
         gbps = c["bytes"] / (fused_ms[i] * 1e-3) / 1e9
         e = {"GBps": round(gbps, 1), "frac_of_hbm": round(gbps / peak, 3), "ms": round(float(fused_ms[i]), 4),
-             "algo_bytes": c["bytes"], "fusion_groups": c["groups"], "kernels": c["kernels"],
+             "algo_bytes": c["bytes"], "plan": c["plan_kind"], "fusion_groups": c["groups"], "kernels": c["kernels"],
              "plan_ms": round(c["plan_ms"], 1),
              "kernel_us": {k: round(v[0], 2) for k, v in kstats[c["name"]].items()},
              "kernel_frac_of_hbm": {k: round(v[1] / (v[0] * 1e-6) / 1e9 / peak, 3) for k, v in kstats[c["name"]].items()}}
@@ -394,6 +409,9 @@ def main():
             e.update({"unfused_GBps": round(c["bytes"] / (base_ms[i] * 1e-3) / 1e9, 1),
                       "unfused_kernels": len(c["base"].info["kernels"]), "speedup_vs_unfused": round(sp, 3)})
             speedups.append(sp)
+        if model_ms is not None and c["model"]:
+            e.update({"model_plan_GBps": round(c["bytes"] / (model_ms[i] * 1e-3) / 1e9, 1),
+                      "model_plan_kernels": len(c["model"].info["kernels"])})
         suite[c["name"]] = e
     geo = float(math.exp(np.mean(np.log(speedups)))) if speedups else None
 

@@ -8,6 +8,7 @@
 
 #include <cstdlib>
 #include <cstring>
+#include <optional>
 #include <string>
 
 #include "json.hpp"
@@ -215,7 +216,11 @@ ordered_json dispatch(const std::string& fn, const ordered_json& a) {
     o.ms_cfg = ms_cfg(a);
     o.cost_cfg = cost_cfg(a);
     o.emit_cfg.shared_limit_bytes = o.cost_cfg.shared_limit_bytes;
-    PlanResult r = run_plan(g, bm_arg(a), o);
+    // Execution-based scores from measured kernel times (pipeline.cpp
+    // CsvExecutionEvaluator, the CLI's --kernel-times CSV).
+    std::optional<CsvExecutionEvaluator> ev;
+    if (a.contains("kernel_times_csv")) ev = CsvExecutionEvaluator::from_csv_text(a["kernel_times_csv"].get<std::string>());
+    PlanResult r = run_plan(g, bm_arg(a), o, ev ? &*ev : nullptr);
     return {{"plan", ordered_json::parse(plan_to_json(r))},
             {"fused", ordered_json::parse(print_graph(r.fused))},
             {"report_text", report_to_text(r.report)}};

@@ -57,8 +57,12 @@ int stitch_executor_create(const char* fused_graph_json, const char* options_jso
     if (o.has("smem_limit_bytes")) opts.codegen.max_smem = static_cast<int>(o.at("smem_limit_bytes").as_int());
     if (o.has("allow_row")) opts.codegen.allow_row = o.at("allow_row").as_bool();
     if (o.has("num_sms")) opts.codegen.num_sms = static_cast<int>(o.at("num_sms").as_int());
+    if (o.has("row_prefetch")) opts.codegen.row_prefetch = o.at("row_prefetch").as_bool();
+    if (o.has("tma_double_buffer")) opts.codegen.tma_double_buffer = o.at("tma_double_buffer").as_bool();
     if (o.has("chunking")) opts.chunking = o.at("chunking").as_bool();
     if (o.has("chunk_l2_bytes")) opts.chunk_l2_bytes = o.at("chunk_l2_bytes").as_int();
+    if (o.has("chunk_pipeline")) opts.chunk_pipeline = o.at("chunk_pipeline").as_bool();
+    if (o.has("chunk_ring")) opts.chunk_ring = static_cast<int>(o.at("chunk_ring").as_int());
     if (o.has("chunk_fill")) opts.chunk_fill = o.at("chunk_fill").as_bool();
     if (o.has("max_chunks")) opts.max_chunks = static_cast<int>(o.at("max_chunks").as_int());
     Graph g = parse_graph(fused_graph_json);

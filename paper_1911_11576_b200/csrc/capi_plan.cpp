@@ -3,6 +3,7 @@
 // stitch_free. Errors: return code != 0 and stitch_last_error() describes it.
 #include <cstdlib>
 #include <cstring>
+#include <optional>
 #include <string>
 
 #include "host/pipeline.hpp"
@@ -117,6 +118,17 @@ json::Value plan_result_json(const Graph& g, const PlanResult& r) {
   t.set("ilp_rounds", r.timings.ilp_rounds);
   out.set("timings", t);
   return out;
+}
+
+// run_plan with the options object; "kernel_times_csv" (name,kernel_us rows:
+// op ids and '+'-joined pattern op ids) plugs in the CSV execution
+// evaluator, which the executor's measured kernel times feed
+// (paper_1911_11576_b200/tuning.py; reference pipeline.cpp
+// CsvExecutionEvaluator).
+json::Value run_plan_json(const Graph& g, const json::Value& a) {
+  std::optional<CsvExecutionEvaluator> ev;
+  if (a.has("kernel_times_csv")) ev = CsvExecutionEvaluator::from_csv_text(a.at("kernel_times_csv").as_string());
+  return plan_result_json(g, run_plan(g, bm_of(a), plan_options(a), ev ? &*ev : nullptr));
 }
 
 // Same function names and JSON shapes as oracle/ref_driver.cpp, so parity
@@ -284,7 +296,7 @@ json::Value dispatch(const std::string& fn, const json::Value& a) {
     out.set("edges_equal", dependence_edges(f) == dependence_edges(g));
     return out;
   }
-  if (fn == "plan") return plan_result_json(g, run_plan(g, bm_of(a), plan_options(a)));
+  if (fn == "plan") return run_plan_json(g, a);
   throw GraphError("unknown function: " + fn);
 }
 
@@ -313,8 +325,7 @@ int stitch_plan_graph(const char* graph_json, const char* options_json, char** r
   try {
     json::Value opts = options_json && *options_json ? json::parse(options_json) : json::Value::object();
     Graph g = parse_graph(graph_json);
-    PlanResult r = run_plan(g, bm_of(opts), plan_options(opts));
-    *result_json = dup(plan_result_json(g, r).dump());
+    *result_json = dup(run_plan_json(g, opts).dump());
     return 0;
   } catch (const InternalError& e) {
     g_error = std::string("internal error: ") + e.what();

@@ -97,6 +97,7 @@ struct Component {
   int64_t slab_floats = 0;
   bool tma = false;
   bool dbuf = false;          // external TMA tiles double-buffered (prefetch the next row)
+  bool prefetch = false;      // register-loaded row inputs prefetched one row ahead
   int64_t ext_floats = 0;     // floats of one copy of the external staged tiles
   std::vector<int> cross, post, free_out;
   int64_t max_grid = 1;
@@ -139,6 +140,9 @@ class Builder {
   void emit_row(Component& c, const std::string& lo, const std::string& n, const std::string& cta_rank);
   void emit_row_finalize(std::vector<Component*>& comps);
   void emit_sectioned(const std::vector<int>& members);
+
+  bool reg_input(const Component& c, int v) const;
+  void emit_row_load(int v, const std::string& dst, const std::string& row, const Layout& L, int NT);
 
   // ROW emission state
   std::string row_access(const Component& c, int o, int v, const std::string& it, const std::string& u,
@@ -478,7 +482,7 @@ bool Builder::plan_row(Component& c) {
     for (int v = 0; v < N; ++v)
       if (c.staged[v] && vals_[v].external) tma_ok = tma_ok && prod(vals_[v].dims, k) % 4 == 0;
     c.tma = tma_ok && std::any_of(inputs_.begin(), inputs_.end(), [&](int v) { return c.staged[v] != 0; });
-    if (c.tma && (c.slab_floats + c.ext_floats + 32 + 8) * 4 <= opts_.max_smem) {
+    if (opts_.tma_double_buffer && c.tma && (c.slab_floats + c.ext_floats + 32 + 8) * 4 <= opts_.max_smem) {
       c.dbuf = true;
       c.slab_floats += c.ext_floats;
     }
@@ -487,6 +491,12 @@ bool Builder::plan_row(Component& c) {
   if (c.cta ? slab_bytes > opts_.max_smem : slab_bytes * 8 > opts_.max_smem) return false;
   c.scheme = "row";
   c.max_grid = c.cta ? c.R : (c.R + 7) / 8;
+  // Prefetch the next row's register tiles when the extra registers fit.
+  int64_t pf_regs = 0;
+  for (int v : inputs_)
+    if (c.cls[v] == Cls::kRowed && !c.staged[v] && prod(vals_[v].dims, k) > 1 && reg_input(c, v))
+      pf_regs += layout(prod(vals_[v].dims, k), c.NT).elems();
+  c.prefetch = opts_.row_prefetch && pf_regs > 0 && pf_regs <= 32;
   return true;
 }
 
@@ -668,6 +678,41 @@ std::string Builder::row_access(const Component& c, int o, int v, const std::str
   return at(o, oc);
 }
 
+// A rowed external input some member reads at the identity element (so it is
+// loaded once per row into registers).
+bool Builder::reg_input(const Component& c, int v) const {
+  for (int m : vals_[v].consumers) {
+    if (std::find(c.members.begin(), c.members.end(), m) == c.members.end()) continue;
+    const OpNode& op = *vals_[m].node;
+    if (op.type == OpType::kReduce) return true;
+    if (op.type == OpType::kElementwise && (op.elem_name != "broadcast" || identity_broadcast(v, m, c.k))) return true;
+  }
+  return false;
+}
+
+// Loads this thread's elements of row `row` of input v into register array
+// `dst` (128-bit streaming loads when the row extent allows).
+void Builder::emit_row_load(int v, const std::string& dst, const std::string& row, const Layout& L, int NT) {
+  const int64_t S = L.S;
+  ln("#pragma unroll");
+  open("for (int it = 0; it < " + std::to_string(L.iters) + "; ++it)");
+  ln("const int lin = (it * " + std::to_string(NT) + " + t) * " + std::to_string(L.vec) + ";");
+  if (L.guard) open("if (lin < " + std::to_string(S) + ")");
+  const std::string src = in_ptr(v) + " + (" + row + ") * " + std::to_string(S) + "LL + lin";
+  if (L.vec == 4) {
+    ln("const float4 q = stitch_dev::ld4_stream(" + src + ");");
+    ln(dst + "[it * 4 + 0] = q.x; " + dst + "[it * 4 + 1] = q.y; " + dst + "[it * 4 + 2] = q.z; " + dst + "[it * 4 + 3] = q.w;");
+  } else {
+    for (int u = 0; u < L.vec; ++u)
+      ln(dst + "[it * " + std::to_string(L.vec) + " + " + std::to_string(u) + "] = __ldg(" + src + " + " + std::to_string(u) + ");");
+  }
+  if (L.guard) {
+    close();
+    ln("else { for (int u = 0; u < " + std::to_string(L.vec) + "; ++u) " + dst + "[it * " + std::to_string(L.vec) + " + u] = 0.0f; }");
+  }
+  close();
+}
+
 void Builder::emit_row(Component& c, const std::string& lo, const std::string& n, const std::string& cta_rank) {
   const int k = c.k;
   const int NT = c.NT;
@@ -746,6 +791,18 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
       close();
     }
   }
+  if (c.prefetch) {
+    for (int v : inputs_)
+      if (c.cls[v] == Cls::kRowed && !c.staged[v] && prod(vals_[v].dims, k) > 1 && reg_input(c, v)) {
+        const Layout L = layout(prod(vals_[v].dims, k), NT);
+        ln("float pf" + std::to_string(v) + "[" + std::to_string(L.elems()) + "];  // next row of " + vals_[v].id);
+      }
+    open("if (" + rlo + " + g0 < " + rhi + ")");
+    for (int v : inputs_)
+      if (c.cls[v] == Cls::kRowed && !c.staged[v] && prod(vals_[v].dims, k) > 1 && reg_input(c, v))
+        emit_row_load(v, "pf" + std::to_string(v), rlo + " + g0", layout(prod(vals_[v].dims, k), NT), NT);
+    close();
+  }
   open("for (long long row = " + rlo + " + g0; row < " + rhi + "; row += gstride" + (c.dbuf ? ", buf ^= 1" : "") + ")");
   reg_.clear();
   scalar_.clear();
@@ -787,6 +844,8 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
   }
 
   // Register loads of rowed inputs read at identity by elementwise ops.
+  // With prefetching (row_pf), the next row's tiles are already in flight in
+  // pf<v> while this row computes: the loop renames pf -> r and re-issues.
   for (int v : inputs_) {
     if (c.cls[v] != Cls::kRowed || c.staged[v]) continue;
     const int64_t S = prod(vals_[v].dims, k);
@@ -796,35 +855,24 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
       scalar_[v] = s;
       continue;
     }
-    bool ident_use = false;
-    for (int m : vals_[v].consumers) {
-      if (std::find(c.members.begin(), c.members.end(), m) == c.members.end()) continue;
-      const OpNode& op = *vals_[m].node;
-      if (op.type == OpType::kReduce) ident_use = true;
-      if (op.type == OpType::kElementwise && (op.elem_name != "broadcast" || identity_broadcast(v, m, k)))
-        ident_use = true;
-    }
-    if (!ident_use) continue;
-    Layout L = layout(S, NT);
-    std::string r = "r" + std::to_string(v);
+    if (!reg_input(c, v)) continue;
+    const Layout L = layout(S, NT);
+    const std::string r = "r" + std::to_string(v);
     ln("float " + r + "[" + std::to_string(L.elems()) + "];  // " + vals_[v].id);
-    ln("#pragma unroll");
-    open("for (int it = 0; it < " + std::to_string(L.iters) + "; ++it)");
-    ln("const int lin = (it * " + std::to_string(NT) + " + t) * " + std::to_string(L.vec) + ";");
-    if (L.guard) open("if (lin < " + std::to_string(S) + ")");
-    const std::string src = in_ptr(v) + " + row * " + std::to_string(S) + "LL + lin";
-    if (L.vec == 4) {
-      ln("const float4 q = stitch_dev::ld4_stream(" + src + ");");
-      ln(r + "[it * 4 + 0] = q.x; " + r + "[it * 4 + 1] = q.y; " + r + "[it * 4 + 2] = q.z; " + r + "[it * 4 + 3] = q.w;");
+    if (c.prefetch) {
+      ln("#pragma unroll");
+      ln("for (int e = 0; e < " + std::to_string(L.elems()) + "; ++e) " + r + "[e] = pf" + std::to_string(v) + "[e];");
     } else {
-      for (int u = 0; u < L.vec; ++u) ln(r + "[it * " + std::to_string(L.vec) + " + " + std::to_string(u) + "] = __ldg(" + src + " + " + std::to_string(u) + ");");
+      emit_row_load(v, r, "row", L, NT);
     }
-    if (L.guard) {
-      close();
-      ln("else { for (int u = 0; u < " + std::to_string(L.vec) + "; ++u) " + r + "[it * " + std::to_string(L.vec) + " + u] = 0.0f; }");
-    }
-    close();
     reg_[v] = r;
+  }
+  if (c.prefetch) {
+    open("if (row + gstride < " + rhi + ")");
+    for (int v : inputs_)
+      if (c.cls[v] == Cls::kRowed && !c.staged[v] && prod(vals_[v].dims, k) > 1 && reg_input(c, v))
+        emit_row_load(v, "pf" + std::to_string(v), "row + gstride", layout(prod(vals_[v].dims, k), NT), NT);
+    close();
   }
 
   auto emit_elementwise_loop = [&](int m, const Layout& L, const std::function<std::string(const std::string&, const std::string&)>& body_fn) {

@@ -57,6 +57,12 @@ struct CodegenOptions {
   int num_sms = 148;
   int max_smem = 232448 - 1024;  // per-CTA opt-in limit minus a static-smem margin
   bool allow_row = true;         // false forces SECTIONED (tests)
+  // Measured on B200 (scripts/time_graph.py): both lose to the occupancy
+  // they cost on the bench configs (layernorm 18.4 -> 24.5 us with
+  // prefetch; GRU 139 -> 170 us with a double buffer at 1 CTA/SM), so they
+  // are opt-in.
+  bool row_prefetch = false;      // prefetch the next row's register tiles
+  bool tma_double_buffer = false; // double-buffer external TMA row tiles
 };
 
 // `constants` maps body-parameter ids whose value is a known scalar constant

@@ -33,6 +33,9 @@ struct CudaApi {
   STITCH_CU_FN(cuMemcpyDtoHAsync)
   STITCH_CU_FN(cuMemcpyDtoDAsync)
   STITCH_CU_FN(cuStreamSynchronize)
+  STITCH_CU_FN(cuStreamCreate)
+  STITCH_CU_FN(cuStreamDestroy)
+  STITCH_CU_FN(cuStreamWaitEvent)
   STITCH_CU_FN(cuEventCreate)
   STITCH_CU_FN(cuEventDestroy)
   STITCH_CU_FN(cuEventRecord)
@@ -83,6 +86,9 @@ struct CudaApi {
     STITCH_CU_LOAD(cuMemcpyDtoHAsync, "cuMemcpyDtoHAsync_v2")
     STITCH_CU_LOAD(cuMemcpyDtoDAsync, "cuMemcpyDtoDAsync_v2")
     STITCH_CU_LOAD(cuStreamSynchronize, "cuStreamSynchronize")
+    STITCH_CU_LOAD(cuStreamCreate, "cuStreamCreate")
+    STITCH_CU_LOAD(cuStreamDestroy, "cuStreamDestroy_v2")
+    STITCH_CU_LOAD(cuStreamWaitEvent, "cuStreamWaitEvent")
     STITCH_CU_LOAD(cuEventCreate, "cuEventCreate")
     STITCH_CU_LOAD(cuEventDestroy, "cuEventDestroy_v2")
     STITCH_CU_LOAD(cuEventRecord, "cuEventRecord")

@@ -125,6 +125,8 @@ Executor::~Executor() {
   if (!device_ready_) return;
   CudaApi& cu = CudaApi::get();
   if (graph_exec_) cu.cuGraphExecDestroy(static_cast<CUgraphExec>(graph_exec_));
+  for (void* e : lane_events_) cu.cuEventDestroy(static_cast<CUevent>(e));
+  for (void* st : lanes_) cu.cuStreamDestroy(static_cast<CUstream>(st));
   for (KernelInst& k : kernels_)
     if (k.module) cu.cuModuleUnload(static_cast<CUmodule>(k.module));
   if (arena_) cu.cuMemFree(arena_);
@@ -301,7 +303,10 @@ void Executor::plan_chunks() {
       }
       seg.chunks = best;
       if (best > 1)
-        for (int b : local) bufs_[b].chunks = best;
+        for (int b : local) {
+          bufs_[b].chunks = best;
+          bufs_[b].ring = opts_.chunk_pipeline ? std::min(best, std::max(1, opts_.chunk_ring)) : 1;
+        }
     }
     segments_.push_back(seg);
   }
@@ -387,69 +392,128 @@ void Executor::init_device() {
     if (k.spec.cooperative) k.grid = static_cast<int>(std::min<int64_t>(k.grid, static_cast<int64_t>(sms_) * 32));
   }
   cubins_tmp_.clear();
+  int lanes = 0, nev = 0;
+  for (const Segment& sg : segments_)
+    if (sg.chunks > 1 && sg.last > sg.first) {
+      lanes = std::max(lanes, sg.last - sg.first + 1);
+      nev += 1 + (sg.last - sg.first + 1) * sg.chunks;
+    }
+  for (int j = 0; j < lanes; ++j) {
+    CUstream st;
+    cu_check(cu.cuStreamCreate(&st, CU_STREAM_NON_BLOCKING), "lane stream");
+    lanes_.push_back(st);
+  }
+  for (int e = 0; e < nev; ++e) {
+    CUevent x;
+    cu_check(cu.cuEventCreate(&x, CU_EVENT_DISABLE_TIMING), "lane event");
+    lane_events_.push_back(x);
+  }
   device_ready_ = true;
+}
+
+void Executor::launch_one(int i, int c, int chunks, const void* const* inputs, void* const* outputs, void* stream) {
+  CudaApi& cu = CudaApi::get();
+  // Address of buffer b as seen by chunk c: a chunk-local buffer holds
+  // `ring` chunk slots and kernels index rows absolutely, so chunk c's slot
+  // base is shifted back by c chunks.
+  auto addr = [&](int b) -> CUdeviceptr {
+    const ValueBuf& x = bufs_[b];
+    if (x.kind == ValueBuf::kInput) return reinterpret_cast<CUdeviceptr>(inputs[x.slot]);
+    if (x.kind == ValueBuf::kOutput) return reinterpret_cast<CUdeviceptr>(outputs[x.slot]);
+    if (x.chunks <= 1) return arena_ + x.offset;
+    const CUdeviceptr cb = static_cast<CUdeviceptr>(x.chunk_bytes());
+    return arena_ + x.offset + static_cast<CUdeviceptr>(c % x.ring) * cb - static_cast<CUdeviceptr>(c) * cb;
+  };
+  KernelInst& k = kernels_[i];
+  CUdeviceptr vals[64];
+  long long rng[2];
+  void* args[66];
+  int na = 0;
+  for (int b : k.in_bufs) vals[na++] = addr(b);
+  for (int b : k.out_bufs) vals[na++] = addr(b);
+  vals[na++] = ws_ + k.ws_off * 4;
+  vals[na++] = sync_ + k.sync_off * 4;
+  if (na > 64) throw std::runtime_error("kernel " + k.spec.name + " has too many arguments");
+  for (int a = 0; a < na; ++a) args[a] = &vals[a];
+  int grid = k.grid;
+  rng[0] = rng[1] = 0;
+  if (k.spec.chunkable) {
+    const int64_t rows = k.spec.rows / chunks;
+    rng[0] = static_cast<long long>(rows * c);
+    rng[1] = static_cast<long long>(rows * (c + 1));
+    if (chunks > 1) {
+      const int64_t need = (rows + k.spec.rows_per_cta - 1) / k.spec.rows_per_cta;
+      grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(grid, need)));
+    }
+  }
+  args[na] = &rng[0];
+  args[na + 1] = &rng[1];
+  CUlaunchConfig cfg;
+  std::memset(&cfg, 0, sizeof cfg);
+  cfg.gridDimX = grid;
+  cfg.gridDimY = cfg.gridDimZ = 1;
+  cfg.blockDimX = k.spec.block;
+  cfg.blockDimY = cfg.blockDimZ = 1;
+  cfg.sharedMemBytes = k.spec.smem_bytes;
+  cfg.hStream = static_cast<CUstream>(stream);
+  CUlaunchAttribute attr[1];
+  if (k.spec.cooperative) {
+    attr[0].id = CU_LAUNCH_ATTRIBUTE_COOPERATIVE;
+    attr[0].value.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  cu_check(cu.cuLaunchKernelEx(&cfg, static_cast<CUfunction>(k.fn), args, nullptr), k.spec.name.c_str());
 }
 
 void Executor::launch_all(const void* const* inputs, void* const* outputs, void* stream, std::vector<void*>* events) {
   CudaApi& cu = CudaApi::get();
-  // Address of buffer b as seen by chunk c: a chunk-local buffer holds one
-  // chunk, and kernels index rows absolutely, so shift its base back.
-  auto addr = [&](int b, int c) -> CUdeviceptr {
-    const ValueBuf& x = bufs_[b];
-    if (x.kind == ValueBuf::kInput) return reinterpret_cast<CUdeviceptr>(inputs[x.slot]);
-    if (x.kind == ValueBuf::kOutput) return reinterpret_cast<CUdeviceptr>(outputs[x.slot]);
-    return arena_ + x.offset - static_cast<CUdeviceptr>(c) * static_cast<CUdeviceptr>(x.arena_bytes() * (x.chunks > 1));
-  };
-  std::vector<CUdeviceptr> vals;
-  std::vector<long long> rng(2);
-  std::vector<void*> args;
+  CUstream s0 = static_cast<CUstream>(stream);
   int launch = 0;
-  for (const Segment& sg : segments_)
+  size_t ev = 0;  // next lane event
+  auto next_event = [&]() { return static_cast<CUevent>(lane_events_.at(ev++)); };
+  for (const Segment& sg : segments_) {
+    const int m = sg.last - sg.first + 1;
+    const bool pipelined = !events && sg.chunks > 1 && m > 1 && opts_.chunk_pipeline;
+    if (!pipelined) {
+      for (int c = 0; c < sg.chunks; ++c)
+        for (int i = sg.first; i <= sg.last; ++i, ++launch) {
+          if (events) cu_check(cu.cuEventRecord(static_cast<CUevent>((*events)[2 * launch]), s0), "event");
+          launch_one(i, c, sg.chunks, inputs, outputs, stream);
+          if (events) cu_check(cu.cuEventRecord(static_cast<CUevent>((*events)[2 * launch + 1]), s0), "event");
+        }
+      continue;
+    }
+    // Fork: every lane starts after what s0 has queued so far.
+    CUevent fork = next_event();
+    cu_check(cu.cuEventRecord(fork, s0), "fork");
+    for (int j = 0; j < m; ++j) cu_check(cu.cuStreamWaitEvent(static_cast<CUstream>(lanes_.at(j)), fork, 0), "fork wait");
+    std::vector<CUevent> done(static_cast<size_t>(m) * sg.chunks);
+    int ring = 1 << 30;
+    for (const ValueBuf& b : bufs_)
+      if (b.chunks > 1 && b.first >= sg.first && b.last <= sg.last) ring = std::min(ring, b.ring);
     for (int c = 0; c < sg.chunks; ++c)
-      for (int i = sg.first; i <= sg.last; ++i, ++launch) {
-        KernelInst& k = kernels_[i];
-        vals.clear();
-        for (int b : k.in_bufs) vals.push_back(addr(b, c));
-        for (int b : k.out_bufs) vals.push_back(addr(b, c));
-        vals.push_back(ws_ + k.ws_off * 4);
-        vals.push_back(sync_ + k.sync_off * 4);
-        const int64_t rows = k.spec.chunkable ? k.spec.rows / sg.chunks : 0;
-        rng[0] = static_cast<long long>(rows * c);
-        rng[1] = static_cast<long long>(rows * (c + 1));
-        if (!k.spec.chunkable) rng[0] = rng[1] = 0;
-        args.clear();
-        for (CUdeviceptr& v : vals) args.push_back(&v);
-        args.push_back(&rng[0]);
-        args.push_back(&rng[1]);
-        int grid = k.grid;
-        if (sg.chunks > 1) {
-          const int64_t need = (rows + k.spec.rows_per_cta - 1) / k.spec.rows_per_cta;
-          grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(grid, need)));
-        }
-        if (k.spec.chunkable && sg.chunks == 1) rng[1] = k.spec.rows;
-        CUlaunchConfig cfg;
-        std::memset(&cfg, 0, sizeof cfg);
-        cfg.gridDimX = grid;
-        cfg.gridDimY = cfg.gridDimZ = 1;
-        cfg.blockDimX = k.spec.block;
-        cfg.blockDimY = cfg.blockDimZ = 1;
-        cfg.sharedMemBytes = k.spec.smem_bytes;
-        cfg.hStream = static_cast<CUstream>(stream);
-        CUlaunchAttribute attr[1];
-        if (k.spec.cooperative) {
-          attr[0].id = CU_LAUNCH_ATTRIBUTE_COOPERATIVE;
-          attr[0].value.cooperative = 1;
-          cfg.attrs = attr;
-          cfg.numAttrs = 1;
-        }
-        if (events) cu_check(cu.cuEventRecord(static_cast<CUevent>((*events)[2 * launch]), static_cast<CUstream>(stream)), "event");
-        cu_check(cu.cuLaunchKernelEx(&cfg, static_cast<CUfunction>(k.fn), args.data(), nullptr), k.spec.name.c_str());
-        if (events) cu_check(cu.cuEventRecord(static_cast<CUevent>((*events)[2 * launch + 1]), static_cast<CUstream>(stream)), "event");
+      for (int j = 0; j < m; ++j, ++launch) {
+        CUstream lane = static_cast<CUstream>(lanes_[j]);
+        if (j > 0) cu_check(cu.cuStreamWaitEvent(lane, done[(j - 1) * sg.chunks + c], 0), "producer wait");
+        // ring slot reuse: chunk c - ring must have left the whole chain
+        if (j == 0 && c >= ring) cu_check(cu.cuStreamWaitEvent(lane, done[(m - 1) * sg.chunks + c - ring], 0), "ring wait");
+        launch_one(sg.first + j, c, sg.chunks, inputs, outputs, lane);
+        CUevent e = next_event();
+        cu_check(cu.cuEventRecord(e, lane), "done");
+        done[j * sg.chunks + c] = e;
       }
-  for (auto [slot, b] : output_copies_)
-    cu_check(cu.cuMemcpyDtoDAsync(reinterpret_cast<CUdeviceptr>(outputs[slot]), addr(b, 0), output_bytes_[slot],
-                                  static_cast<CUstream>(stream)),
+    // Join: s0 continues after every lane's last chunk.
+    for (int j = 0; j < m; ++j) cu_check(cu.cuStreamWaitEvent(s0, done[j * sg.chunks + sg.chunks - 1], 0), "join");
+  }
+  for (auto [slot, b] : output_copies_) {
+    const ValueBuf& x = bufs_[b];
+    CUdeviceptr src = x.kind == ValueBuf::kInput ? reinterpret_cast<CUdeviceptr>(inputs[x.slot])
+                      : x.kind == ValueBuf::kOutput ? reinterpret_cast<CUdeviceptr>(outputs[x.slot])
+                                                    : arena_ + x.offset;
+    cu_check(cu.cuMemcpyDtoDAsync(reinterpret_cast<CUdeviceptr>(outputs[slot]), src, output_bytes_[slot], s0),
              "output copy");
+  }
 }
 
 void Executor::run(const void* const* inputs, void* const* outputs, void* stream) {

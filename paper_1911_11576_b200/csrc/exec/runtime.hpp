@@ -30,8 +30,17 @@ struct ExecOptions {
   // every chunk, so it stays in L2 and is overwritten before write-back.
   int64_t chunk_l2_bytes = 24ll << 20;  // target intermediate bytes per chunk (L2 is 126 MB)
   int max_chunks = 64;
-  bool chunking = true;
+  // Measured on B200: chunked launches lose to whole-tensor launches on the
+  // bench configs (softmax 43 -> 51 us, encoder 145 -> 172 us: per-launch
+  // ramp and tail dominate the L2 savings), so chunking is opt-in.
+  bool chunking = false;
   bool chunk_fill = true;  // require enough rows per chunk to fill every SM (tests force small chunks)
+  // Pipelined chunks: kernel j of a chunked segment runs on its own stream,
+  // chunk c waiting only for kernel j-1's chunk c, so kernel j's chunk c
+  // overlaps kernel j-1's chunk c+1 (tails filled); intermediates use a ring
+  // of `chunk_ring` chunk slots.
+  bool chunk_pipeline = true;
+  int chunk_ring = 2;
   CodegenOptions codegen;
 };
 
@@ -47,8 +56,10 @@ struct ValueBuf {
   int slot = -1;        // input / output position
   int64_t offset = 0;   // arena byte offset
   int first = -1, last = -1;  // producing / last consuming kernel
-  int chunks = 1;             // > 1: chunk-local intermediate, arena holds bytes / chunks
-  int64_t arena_bytes() const { return bytes / chunks; }
+  int chunks = 1;             // > 1: chunk-local intermediate, arena holds `ring` chunk slots
+  int ring = 1;
+  int64_t chunk_bytes() const { return bytes / chunks; }
+  int64_t arena_bytes() const { return chunk_bytes() * (chunks > 1 ? ring : 1); }
 };
 
 struct Segment {  // kernels [first, last] in launch order, run chunk by chunk when chunks > 1
@@ -89,6 +100,7 @@ class Executor {
   void init_device();
   void plan_chunks();
   void launch_all(const void* const* inputs, void* const* outputs, void* stream, std::vector<void*>* events);
+  void launch_one(int i, int c, int chunks, const void* const* inputs, void* const* outputs, void* stream);
 
   Graph g_;
   ExecOptions opts_;
@@ -97,6 +109,8 @@ class Executor {
   std::vector<KernelInst> kernels_;
   std::vector<Segment> segments_;
   int launches_per_run_ = 0;
+  std::vector<void*> lanes_;        // CUstreams for pipelined chunk lanes
+  std::vector<void*> lane_events_;  // CUevents: [segment-local kernel j][chunk c] done, plus fork/join
   std::vector<std::string> input_ids_, output_ids_;
   std::vector<int64_t> input_bytes_, output_bytes_;
   std::vector<std::vector<int64_t>> input_dims_, output_dims_;

@@ -8,6 +8,7 @@ FNV-1a hash of the full kernel source plus the NVRTC options
 """
 
 from . import runtime as rt
+from . import tuning
 from . import workloads as W
 
 
@@ -22,6 +23,8 @@ def plans(full=True, small=True):
             sizes.append(("small", W.SMALL[name]))
         for size, kw in sizes:
             g = fn(**kw)
+            if size == "full" and tuning.load(name) is not None:
+                out.append(("%s/%s/exec" % (name, size), tuning.config_plan(name, g)[0]["fused"]))
             for lim_tag, lim in (("b200", W.B200_SHARED_LIMIT), ("ref48k", W.REFERENCE_SHARED_LIMIT)):
                 out.append(("%s/%s/%s" % (name, size, lim_tag), rt.plan(g, shared_limit_bytes=lim)["fused"]))
             out.append(("%s/%s/unfused" % (name, size), g))

@@ -23,10 +23,11 @@ for name in a.configs.split(","):
     if a.unfused:
         graphs.append(("unfused", g))
     for tag, fg in graphs:
-        ex = rt.Executor(fg, use_graph=False)
+        ex = rt.Executor(fg, use_graph=False, chunking=(tag == "fused"))
         ins = [torch.randn(t["dims"], device="cuda") for t in ex.info["inputs"]]
         outs = [torch.empty(t["dims"], device="cuda") for t in ex.info["outputs"]]
         for _ in range(a.iters):
             ex.run(ins, outs, stream=torch.cuda.current_stream().cuda_stream)
         torch.cuda.synchronize()
-        print(name, tag, [k["name"] for k in ex.info["kernels"]], flush=True)
+        seq = [k for s in ex.info["schedule"] for _ in range(s["chunks"]) for k in s["kernels"]]
+        print(name, tag, seq, flush=True)

@@ -13,6 +13,7 @@ import pytest
 from oracle import executor as orc
 from oracle import tolerance
 from paper_1911_11576_b200 import runtime as rt
+from paper_1911_11576_b200 import tuning
 from paper_1911_11576_b200 import workloads as W
 
 pytestmark = pytest.mark.gpu
@@ -91,14 +92,20 @@ def test_ragged_parity(name, kw):
 
 
 @pytest.mark.parametrize("name", list(W.CONFIGS))
-def test_full_size_row_sampled(name):
+@pytest.mark.parametrize("plan_kind", ["exec", "model"])
+def test_full_size_row_sampled(name, plan_kind):
     """Full BASELINE size on the GPU; batch items [0, 2) and the last two
     are checked against the oracle on those items (every config is
     independent per batch item); per-shard column reductions (encoder's
     dbias) against an fp64 reduction of the full input."""
     g = W.CONFIGS[name]()
     batch, rows = W.shard_layout(name)
-    fused = rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT)["fused"]
+    if plan_kind == "exec":
+        res, desc = tuning.config_plan(name, g)
+        assert desc.startswith("execution")
+        fused = res["fused"]
+    else:
+        fused = rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT)["fused"]
     rng = np.random.default_rng(21)
     nodes = {n["id"]: n for n in g["nodes"]}
     ins = {i: rng.standard_normal(nodes[i]["shape"]["dims"], dtype=np.float32) for i in orc.graph_inputs(g)}
@@ -169,16 +176,27 @@ def test_profile_reports_every_kernel():
 def test_chunked_schedule_bit_identical(name):
     """L2-resident chunked launches (intermediates in one-chunk buffers
     reused by every chunk) give bit-identical results to whole-tensor
-    launches at the full BASELINE size (parity with the oracle at full size
-    is test_full_size_row_sampled, which runs chunked by default)."""
+    launches at the full BASELINE size; also with prefetching and
+    double-buffered TMA staging (the opt-in codegen variants)."""
     g = W.CONFIGS[name]()
     fused = rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT)["fused"]
     rng = np.random.default_rng(51)
     nodes = {n["id"]: n for n in g["nodes"]}
     ins = {i: rng.standard_normal(nodes[i]["shape"]["dims"], dtype=np.float32) for i in orc.graph_inputs(g)}
-    ex_c, a = run_device(fused, ins)
+    ex_c, a = run_device(fused, ins, chunking=True)
     assert any(s["chunks"] > 1 for s in ex_c.info["schedule"]), ex_c.info["schedule"]
     ex_n, b = run_device(fused, ins, chunking=False)
     assert all(s["chunks"] == 1 for s in ex_n.info["schedule"])
     for x, y in zip(a, b):
         assert np.array_equal(x, y)
+    _, c = run_device(fused, ins, chunking=True, chunk_pipeline=False, row_prefetch=True)
+    for x, y in zip(c, b):
+        assert np.array_equal(x, y)
+
+
+def test_gru_double_buffer_and_prefetch_variants():
+    g = W.gru(batch=37, n=64)
+    fused = rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT)["fused"]
+    ins = orc.random_inputs(g, seed=52)
+    ex = assert_parity(g, fused, ins, tma_double_buffer=True, row_prefetch=True)
+    assert "tma2" in ex.info["kernels"][0]["scheme"]

@@ -156,3 +156,16 @@ def test_m_of_v_and_scores(ref):
         nodes = ["dot_1", "multiply_1", "exp_1"][: len(per)]
         a, b = both(ref, "score_execution", graph=g, nodes=nodes, per_op_us=per, fused_us=fused)
         assert a == b
+
+
+@pytest.mark.parametrize("name", ["layernorm", "softmax", "gru"])
+def test_execution_based_plans(ref, name):
+    """Execution-based scoring (paper §4.3) from the shipped B200 kernel-time
+    table: the reference planner with the same CSV evaluator selects the same
+    fusion groups. (encoder: tests/golden/plans_exec.json, the reference
+    takes minutes.)"""
+    from paper_1911_11576_b200 import tuning
+    g = W.CONFIGS[name]()
+    csv = tuning.load(name)
+    a, b = both(ref, "plan", graph=g, mode="execution", kernel_times_csv=csv)
+    assert strip_plan(a) == strip_plan(b)
