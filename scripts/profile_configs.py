@@ -9,6 +9,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 from paper_1911_11576_b200 import runtime as rt  # noqa: E402
+from paper_1911_11576_b200 import tuning  # noqa: E402
 from paper_1911_11576_b200 import workloads as W  # noqa: E402
 
 ap = argparse.ArgumentParser()
@@ -19,11 +20,11 @@ a = ap.parse_args()
 torch.cuda.set_device(0)
 for name in a.configs.split(","):
     g = W.CONFIGS[name]()
-    graphs = [("fused", rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT)["fused"])]
+    graphs = [("fused", tuning.config_plan(name, g)[0]["fused"])]
     if a.unfused:
         graphs.append(("unfused", g))
     for tag, fg in graphs:
-        ex = rt.Executor(fg, use_graph=False, chunking=(tag == "fused"))
+        ex = rt.Executor(fg, use_graph=False)
         ins = [torch.randn(t["dims"], device="cuda") for t in ex.info["inputs"]]
         outs = [torch.empty(t["dims"], device="cuda") for t in ex.info["outputs"]]
         for _ in range(a.iters):
