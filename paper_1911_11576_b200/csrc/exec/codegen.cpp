@@ -98,6 +98,7 @@ struct Component {
   bool tma = false;
   bool dbuf = false;          // external TMA tiles double-buffered (prefetch the next row)
   bool prefetch = false;      // register-loaded row inputs prefetched one row ahead
+  std::vector<char> cheap;    // rowed broadcasts of constants / free tensors: recomputed at each use, never stored
   int64_t ext_floats = 0;     // floats of one copy of the external staged tiles
   std::vector<int> cross, post, free_out;
   int64_t max_grid = 1;
@@ -142,12 +143,14 @@ class Builder {
   void emit_sectioned(const std::vector<int>& members);
 
   bool reg_input(const Component& c, int v) const;
+  void emit_row_scalar(const Component& c, int m);
   void emit_row_load(int v, const std::string& dst, const std::string& row, const Layout& L, int NT);
 
   // ROW emission state
   std::string row_access(const Component& c, int o, int v, const std::string& it, const std::string& u,
                          const Layout& L);
   std::map<int, std::string> reg_;  // value -> register array name (per row body)
+  std::map<int, std::string> loop_scalar_;  // value -> scalar of the current fused elementwise loop
   std::map<int, std::string> scalar_;
 
   const Graph& body_;
@@ -491,6 +494,26 @@ bool Builder::plan_row(Component& c) {
   if (c.cta ? slab_bytes > opts_.max_smem : slab_bytes * 8 > opts_.max_smem) return false;
   c.scheme = "row";
   c.max_grid = c.cta ? c.R : (c.R + 7) / 8;
+  // Broadcasts of constants or free (row-independent) tensors read only at
+  // the identity element by elementwise consumers are recomputed at each use
+  // (a literal or an L1-resident gather) instead of occupying registers.
+  c.cheap.assign(N, 0);
+  for (int m : c.members) {
+    const OpNode& op = *vals_[m].node;
+    if (c.cls[m] != Cls::kRowed || op.type != OpType::kElementwise || op.elem_name != "broadcast") continue;
+    const int in = vals_[m].operands[0];
+    if (!(vals_[in].constant || c.cls[in] == Cls::kFree)) continue;
+    if (vals_[m].output || c.staged[m] || prod(vals_[m].dims, k) == 1) continue;
+    bool ok = true;
+    for (int cns : vals_[m].consumers) {
+      if (std::find(c.members.begin(), c.members.end(), cns) == c.members.end()) continue;
+      const OpNode& co = *vals_[cns].node;
+      ok = ok && c.cls[cns] == Cls::kRowed && co.type == OpType::kElementwise &&
+           prod(vals_[cns].dims, k) == prod(vals_[m].dims, k) &&
+           (co.elem_name != "broadcast" || identity_broadcast(m, cns, k));
+    }
+    if (ok && opts_.loop_fusion) c.cheap[m] = 1;
+  }
   // Prefetch the next row's register tiles when the extra registers fit.
   int64_t pf_regs = 0;
   for (int v : inputs_)
@@ -631,6 +654,8 @@ std::string Builder::row_access(const Component& c, int o, int v, const std::str
   const int k = c.k;
   const std::string e = "(" + it + ") * " + std::to_string(L.vec) + " + (" + u + ")";
   const std::string lin = "((" + it + ") * " + std::to_string(c.NT) + " + t) * " + std::to_string(L.vec) + " + (" + u + ")";
+  if (c.cls[o] == Cls::kRowed && !c.cheap.empty() && c.cheap[o])
+    return row_access(c, vals_[o].operands[0], o, it, u, L);
   if (c.cls[o] == Cls::kRowed) {
     const int64_t So = prod(x.dims, k);
     if (So == 1) {
@@ -641,6 +666,8 @@ std::string Builder::row_access(const Component& c, int o, int v, const std::str
     const bool ident = (vals_[v].node->type == OpType::kElementwise &&
                         (vals_[v].node->elem_name != "broadcast" || identity_broadcast(o, v, k)));
     if (ident) {
+      auto ls = loop_scalar_.find(o);
+      if (ls != loop_scalar_.end()) return ls->second;
       auto r = reg_.find(o);
       if (r != reg_.end()) return r->second + "[" + e + "]";
       if (c.staged[o]) return "sm" + std::to_string(o) + "[" + lin + "]";
@@ -676,6 +703,27 @@ std::string Builder::row_access(const Component& c, int o, int v, const std::str
     if (id) return "__ldg(" + in_ptr(o) + " + " + lin + ")";
   }
   return at(o, oc);
+}
+
+// Row-scalar elementwise op (one value per row, S == 1): every thread of the
+// row group holds it.
+void Builder::emit_row_scalar(const Component& c, int m) {
+  const OpNode& op = *vals_[m].node;
+  std::vector<std::string> args;
+  for (int o : vals_[m].operands) {
+    if (vals_[o].constant) {
+      args.push_back(flit(vals_[o].cval));
+    } else if (c.cls[o] == Cls::kRowed) {
+      auto s = scalar_.find(o);
+      args.push_back(s != scalar_.end() ? s->second : "__ldg(" + in_ptr(o) + " + row)");
+    } else {
+      std::vector<std::string> zero(vals_[o].dims.size(), "0");
+      args.push_back(at(o, zero));
+    }
+  }
+  std::string s = fresh("s");
+  ln("const float " + s + " = " + elem_expr(op, args) + ";  // " + vals_[m].id);
+  scalar_[m] = s;
 }
 
 // A rowed external input some member reads at the identity element (so it is
@@ -898,28 +946,118 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
     reg_[m] = r;
   };
 
-  for (int m : c.members) {
+  auto stage_value = [&](int m, const Layout& L, int64_t S) {
+    ln(sync);  // previous readers of this slab region are done
+    ln("#pragma unroll");
+    open("for (int it = 0; it < " + std::to_string(L.iters) + "; ++it)");
+    ln("#pragma unroll");
+    open("for (int u = 0; u < " + std::to_string(L.vec) + "; ++u)");
+    ln("const int lin = (it * " + std::to_string(NT) + " + t) * " + std::to_string(L.vec) + " + u;");
+    std::string val = S == 1 ? scalar_[m] : reg_[m] + "[it * " + std::to_string(L.vec) + " + u]";
+    ln((L.guard ? "if (lin < " + std::to_string(S) + ") " : std::string()) + "sm" + std::to_string(m) + "[lin] = " + val + ";");
+    close();
+    close();
+    ln(sync);
+  };
+  auto in_comp = [&](int x) { return std::find(c.members.begin(), c.members.end(), x) != c.members.end(); };
+
+  for (size_t mi = 0; mi < c.members.size(); ++mi) {
+    const int m = c.members[mi];
     if (c.cls[m] != Cls::kRowed) continue;
     const OpNode& op = *vals_[m].node;
     const int64_t S = prod(vals_[m].dims, k);
     const Layout L = layout(S, NT);
+    if (op.type == OpType::kElementwise && S > 1 && opts_.loop_fusion) {
+      // Aggressive loop fusion (paper §5.1: "merge as many elementwise ops
+      // as possible into a single loop structure"): the run of consecutive
+      // rowed elementwise ops over the same row extent becomes one loop
+      // over this thread's elements; values used only inside the run live
+      // in scalars, only escaping values get register arrays.
+      std::vector<int> grp, hoisted;
+      std::set<int> in_grp;
+      size_t mj = mi;
+      for (; mj < c.members.size(); ++mj) {
+        const int x = c.members[mj];
+        if (c.cls[x] != Cls::kRowed) {
+          bool reads_grp = false;
+          for (int o : vals_[x].operands) reads_grp = reads_grp || in_grp.count(o);
+          if (reads_grp) break;  // e.g. a cross-row reduce of a run value: keep order simple
+          continue;
+        }
+        const OpNode& xo = *vals_[x].node;
+        if (c.cheap[x]) continue;  // recomputed at its uses
+        if (xo.type == OpType::kElementwise && prod(vals_[x].dims, k) == 1) {
+          bool reads_grp = false;
+          for (int o : vals_[x].operands) reads_grp = reads_grp || in_grp.count(o);
+          if (reads_grp) break;
+          hoisted.push_back(x);  // row scalar, independent of the run: emitted before the loop
+          continue;
+        }
+        if (xo.type != OpType::kElementwise || prod(vals_[x].dims, k) != S) break;
+        bool ok = true;
+        for (int o : vals_[x].operands)
+          if (in_grp.count(o) && xo.elem_name == "broadcast" && !identity_broadcast(o, x, k)) ok = false;
+        if (!ok) break;
+        grp.push_back(x);
+        in_grp.insert(x);
+      }
+      for (int x : hoisted) emit_row_scalar(c, x);
+      std::set<int> escapes;
+      for (int g : grp) {
+        bool esc = vals_[g].output || c.staged[g];
+        for (int cns : vals_[g].consumers)
+          if (in_comp(cns) && !in_grp.count(cns)) esc = true;
+        if (esc) escapes.insert(g);
+      }
+      for (int g : grp)
+        if (escapes.count(g)) ln("float r" + std::to_string(g) + "[" + std::to_string(L.elems()) + "];  // " + vals_[g].id);
+      ln("#pragma unroll");
+      open("for (int it = 0; it < " + std::to_string(L.iters) + "; ++it)");
+      ln("#pragma unroll");
+      open("for (int u = 0; u < " + std::to_string(L.vec) + "; ++u)");
+      memo_.emplace_back();
+      if (L.guard) {
+        ln("const int lin_g = (it * " + std::to_string(NT) + " + t) * " + std::to_string(L.vec) + " + u;");
+        open("if (lin_g < " + std::to_string(L.S) + ")");
+      }
+      for (int g : grp) {
+        std::vector<std::string> args;
+        for (int o : vals_[g].operands) args.push_back(row_access(c, o, g, "it", "u", L));
+        const std::string v = "v" + std::to_string(g);
+        ln("const float " + v + " = " + elem_expr(*vals_[g].node, args) + ";  // " + vals_[g].id);
+        loop_scalar_[g] = v;
+        if (escapes.count(g)) ln("r" + std::to_string(g) + "[it * " + std::to_string(L.vec) + " + u] = " + v + ";");
+      }
+      if (L.guard) {
+        close();
+        open("else");
+        for (int g : grp)
+          if (escapes.count(g)) ln("r" + std::to_string(g) + "[it * " + std::to_string(L.vec) + " + u] = 0.0f;");
+        close();
+      }
+      memo_.pop_back();
+      close();
+      close();
+      for (int g : grp) {
+        loop_scalar_.erase(g);
+        if (escapes.count(g)) reg_[g] = "r" + std::to_string(g);
+      }
+      for (int g : grp)
+        if (c.staged[g]) stage_value(g, L, S);
+      // continue after the last fused / hoisted member (skipped non-rowed and
+      // cheap members emit nothing here)
+      size_t last = mi;
+      for (size_t q = mi; q < c.members.size(); ++q)
+        if (in_grp.count(c.members[q]) ||
+            std::find(hoisted.begin(), hoisted.end(), c.members[q]) != hoisted.end())
+          last = q;
+      mi = last;
+      continue;
+    }
+    if (!c.cheap.empty() && c.cheap[m]) continue;
     if (op.type == OpType::kElementwise) {
       if (S == 1) {
-        // row scalar: every thread holds the value
-        std::vector<std::string> args;
-        for (int o : vals_[m].operands) {
-          if (vals_[o].constant) args.push_back(flit(vals_[o].cval));
-          else if (c.cls[o] == Cls::kRowed) {
-            auto s = scalar_.find(o);
-            args.push_back(s != scalar_.end() ? s->second : "__ldg(" + in_ptr(o) + " + row)");
-          } else {
-            std::vector<std::string> zero(vals_[o].dims.size(), "0");
-            args.push_back(at(o, zero));
-          }
-        }
-        std::string s = fresh("s");
-        ln("const float " + s + " = " + elem_expr(op, args) + ";  // " + vals_[m].id);
-        scalar_[m] = s;
+        emit_row_scalar(c, m);
       } else {
         emit_elementwise_loop(m, L, [&](const std::string& it, const std::string& u) {
           std::vector<std::string> args;
@@ -1094,19 +1232,7 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
       spec_.flops += 2 * mnk;
     }
     // Stage computed values that later ops gather from.
-    if (c.staged[m]) {
-      ln(sync);  // previous readers of this slab region are done
-      ln("#pragma unroll");
-      open("for (int it = 0; it < " + std::to_string(L.iters) + "; ++it)");
-      ln("#pragma unroll");
-      open("for (int u = 0; u < " + std::to_string(L.vec) + "; ++u)");
-      ln("const int lin = (it * " + std::to_string(NT) + " + t) * " + std::to_string(L.vec) + " + u;");
-      std::string val = S == 1 ? scalar_[m] : reg_[m] + "[it * " + std::to_string(L.vec) + " + u]";
-      ln((L.guard ? "if (lin < " + std::to_string(S) + ") " : std::string()) + "sm" + std::to_string(m) + "[lin] = " + val + ";");
-      close();
-      close();
-      ln(sync);
-    }
+    if (c.staged[m]) stage_value(m, L, S);
   }
 
   // Cross-row accumulation.
@@ -1464,9 +1590,9 @@ KernelSpec Builder::build() {
     std::string scheme;
     chunked_ = comps.size() == 1 && comps[0].scheme == "row" && comps[0].cross.empty() && comps[0].post.empty() &&
                comps[0].free_out.empty();
+    if (comps.size() == 1 && comps[0].scheme == "row") spec_.rows = comps[0].R;
     if (chunked_) {
       spec_.chunkable = true;
-      spec_.rows = comps[0].R;
       spec_.rows_per_cta = comps[0].cta ? 1 : block / 32;
     }
     for (size_t i = 0; i < comps.size(); ++i) {
@@ -1544,6 +1670,11 @@ KernelSpec Builder::build() {
   spec_.source = head.str() + body_src + "}\n";
   spec_.block = block;
   spec_.smem_bytes = static_cast<int>(smem_floats * 4 + (smem_floats ? 16 : 0));
+  if (!sectioned && comps.size() == 1 && comps[0].scheme == "row" && !comps[0].cta) {
+    // every shared-memory term of a warp-row kernel is per warp
+    spec_.flex_block = true;
+    spec_.smem_per_warp = static_cast<int>((smem_floats * 4 + (block / 32) - 1) / (block / 32));
+  }
   spec_.workspace_floats = ws_floats_;
   spec_.sync_words = (spec_.cooperative || uses_barrier_) ? 2 : 0;
   if (uses_barrier_) spec_.cooperative = true;

@@ -49,6 +49,10 @@ struct KernelSpec {
   // kernel can run any row range [row_lo, row_hi) (trailing kernel args) and
   // touches exactly that range's bytes of every rowed tensor.
   bool chunkable = false;
+  // Warp-per-row kernels read blockDim at run time, so the runtime may launch
+  // them with any warp count <= block; shared memory scales per warp.
+  bool flex_block = false;
+  int smem_per_warp = 0;
   int64_t rows = 0;
   int rows_per_cta = 1;
 };
@@ -62,6 +66,7 @@ struct CodegenOptions {
   // prefetch; GRU 139 -> 170 us with a double buffer at 1 CTA/SM), so they
   // are opt-in.
   bool row_prefetch = false;      // prefetch the next row's register tiles
+  bool loop_fusion = true;        // one loop per run of same-extent elementwise ops (scalars inside)
   bool tma_double_buffer = false; // double-buffer external TMA row tiles
 };
 

@@ -384,11 +384,32 @@ void Executor::init_device() {
     if (k.spec.smem_bytes > 48 * 1024)
       cu_check(cu.cuFuncSetAttribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, k.spec.smem_bytes),
                "smem attribute");
+    k.block = k.spec.block;
+    k.smem = k.spec.smem_bytes;
     int occ = 0;
-    cu_check(cu.cuOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, k.spec.block, k.spec.smem_bytes), "occupancy");
+    cu_check(cu.cuOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, k.block, k.smem), "occupancy");
+    if (k.spec.flex_block) {
+      // Register-limited warp-row kernels: the warp count per CTA that keeps
+      // the most warps resident (finer CTAs fill the register file better).
+      int best_warps = occ * k.block / 32;
+      for (int b = k.spec.block - 32; b >= 64; b -= 32) {
+        const int smem = k.spec.smem_per_warp * (b / 32);
+        int o = 0;
+        cu_check(cu.cuOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, b, smem), "occupancy");
+        if (o * b / 32 > best_warps) {
+          best_warps = o * b / 32;
+          k.block = b;
+          k.smem = smem;
+          occ = o;
+        }
+      }
+    }
     if (occ < 1) throw std::runtime_error("kernel " + k.spec.name + " cannot be resident (block/smem too large)");
     const int64_t resident = static_cast<int64_t>(occ) * sms_;
-    k.grid = static_cast<int>(std::min<int64_t>(std::max(1, k.spec.max_grid), resident));
+    int64_t useful = std::max(1, k.spec.max_grid);
+    if (k.spec.flex_block && k.spec.rows > 0) useful = (k.spec.rows + k.block / 32 - 1) / (k.block / 32);
+    if (k.spec.flex_block && k.spec.rows == 0) useful = static_cast<int64_t>(k.spec.max_grid) * k.spec.block / k.block;
+    k.grid = static_cast<int>(std::min<int64_t>(useful, resident));
     if (k.spec.cooperative) k.grid = static_cast<int>(std::min<int64_t>(k.grid, static_cast<int64_t>(sms_) * 32));
   }
   cubins_tmp_.clear();
@@ -442,7 +463,8 @@ void Executor::launch_one(int i, int c, int chunks, const void* const* inputs, v
     rng[0] = static_cast<long long>(rows * c);
     rng[1] = static_cast<long long>(rows * (c + 1));
     if (chunks > 1) {
-      const int64_t need = (rows + k.spec.rows_per_cta - 1) / k.spec.rows_per_cta;
+      const int rpc = k.spec.flex_block ? k.block / 32 : k.spec.rows_per_cta;
+      const int64_t need = (rows + rpc - 1) / rpc;
       grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(grid, need)));
     }
   }
@@ -452,9 +474,9 @@ void Executor::launch_one(int i, int c, int chunks, const void* const* inputs, v
   std::memset(&cfg, 0, sizeof cfg);
   cfg.gridDimX = grid;
   cfg.gridDimY = cfg.gridDimZ = 1;
-  cfg.blockDimX = k.spec.block;
+  cfg.blockDimX = k.block;
   cfg.blockDimY = cfg.blockDimZ = 1;
-  cfg.sharedMemBytes = k.spec.smem_bytes;
+  cfg.sharedMemBytes = k.smem;
   cfg.hStream = static_cast<CUstream>(stream);
   CUlaunchAttribute attr[1];
   if (k.spec.cooperative) {
@@ -645,8 +667,8 @@ json::Value Executor::describe() const {
     for (const std::string& c : k.spec.composition) comp.push(c);
     e.set("composition", comp);
     e.set("grid", k.grid);
-    e.set("block", k.spec.block);
-    e.set("smem_bytes", k.spec.smem_bytes);
+    e.set("block", k.block ? k.block : k.spec.block);
+    e.set("smem_bytes", k.block ? k.smem : k.spec.smem_bytes);
     e.set("cooperative", k.spec.cooperative);
     e.set("algo_bytes", k.spec.algo_bytes);
     e.set("flops", k.spec.flops);

@@ -73,6 +73,8 @@ struct KernelInst {
   void* module = nullptr;            // CUmodule
   void* fn = nullptr;                // CUfunction
   int grid = 1;
+  int block = 0;                     // launch block (spec.block, or the best warp count for flex kernels)
+  int smem = 0;                      // dynamic shared memory at that block
   int64_t ws_off = 0;                // floats into the workspace pool
   int64_t sync_off = 0;              // u32 words into the sync pool
   bool cache_hit = false;
