@@ -143,6 +143,7 @@ class Builder {
   void emit_sectioned(const std::vector<int>& members);
 
   bool reg_input(const Component& c, int v) const;
+  bool free_vector_access(const Component& c, int o, int v) const;
   void emit_row_scalar(const Component& c, int m);
   void emit_row_load(int v, const std::string& dst, const std::string& row, const Layout& L, int NT);
 
@@ -151,6 +152,7 @@ class Builder {
                          const Layout& L);
   std::map<int, std::string> reg_;  // value -> register array name (per row body)
   std::map<int, std::string> loop_scalar_;  // value -> scalar of the current fused elementwise loop
+  std::map<int, std::string> freevec_;      // free external -> float[4] of the current `it` (fused loop)
   std::map<int, std::string> scalar_;
 
   const Graph& body_;
@@ -694,13 +696,12 @@ std::string Builder::row_access(const Component& c, int o, int v, const std::str
   for (int i = 0; i < k; ++i) full.push_back("0");
   full.insert(full.end(), vc.begin(), vc.end());
   std::vector<std::string> oc = (vals_[v].node->elem_name == "broadcast") ? map_broadcast(o, v, full) : full;
-  // Same-shape free input read at the identity element: vector-friendly index.
-  if (x.external && x.dims == vin && vals_[v].node->elem_name != "broadcast") return "__ldg(" + in_ptr(o) + " + " + lin + ")";
-  if (x.external && vals_[v].node->elem_name == "broadcast" && x.dims == vin) {
-    std::vector<int> mp = broadcast_dim_map(x.node->shape, vals_[v].node->shape);
-    bool id = true;
-    for (size_t i = 0; i < mp.size(); ++i) id = id && mp[i] == static_cast<int>(i) + k;
-    if (id) return "__ldg(" + in_ptr(o) + " + " + lin + ")";
+  // Same-shape free input read at the identity element: vector-friendly index
+  // (a float4 loaded once per `it` by the fused loop when available).
+  if (free_vector_access(c, o, v)) {
+    auto fv = freevec_.find(o);
+    if (fv != freevec_.end()) return fv->second + "[" + u + "]";
+    return "__ldg(" + in_ptr(o) + " + " + lin + ")";
   }
   return at(o, oc);
 }
@@ -724,6 +725,20 @@ void Builder::emit_row_scalar(const Component& c, int m) {
   std::string s = fresh("s");
   ln("const float " + s + " = " + elem_expr(op, args) + ";  // " + vals_[m].id);
   scalar_[m] = s;
+}
+
+// v reads free external o at v's own in-row element (o's dims are v's inner
+// dims and the access is the identity): a row-invariant vector like a bias.
+bool Builder::free_vector_access(const Component& c, int o, int v) const {
+  const Val& x = vals_[o];
+  if (!x.external || c.cls[o] != Cls::kFree || vals_[v].node->type != OpType::kElementwise) return false;
+  std::vector<int64_t> vin(vals_[v].dims.begin() + c.k, vals_[v].dims.end());
+  if (x.dims != vin) return false;
+  if (vals_[v].node->elem_name != "broadcast") return true;
+  std::vector<int> mp = broadcast_dim_map(x.node->shape, vals_[v].node->shape);
+  for (size_t i = 0; i < mp.size(); ++i)
+    if (mp[i] != static_cast<int>(i) + c.k) return false;
+  return true;
 }
 
 // A rowed external input some member reads at the identity element (so it is
@@ -1013,6 +1028,33 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
         if (escapes.count(g)) ln("float r" + std::to_string(g) + "[" + std::to_string(L.elems()) + "];  // " + vals_[g].id);
       ln("#pragma unroll");
       open("for (int it = 0; it < " + std::to_string(L.iters) + "; ++it)");
+      if (L.vec == 4) {
+        // row-invariant vectors (bias, gamma, mask, ...) this run reads at
+        // its own element: one 128-bit L1-cached load per `it`
+        std::set<int> fvs;
+        std::function<void(int, int)> scan = [&](int g, int depth) {
+          for (int o : vals_[g].operands) {
+            if (free_vector_access(c, o, g)) fvs.insert(o);
+            if (depth < 4 && c.cls[o] == Cls::kRowed && !c.cheap.empty() && c.cheap[o]) scan(o, depth + 1);
+          }
+        };
+        for (int g : grp) scan(g, 0);
+        for (int o : fvs) {
+          const std::string f = "fv" + std::to_string(o);
+          ln("float " + f + "[4];");
+          open("");
+          ln("const int lin4 = (it * " + std::to_string(NT) + " + t) * 4;");
+          if (L.guard) open("if (lin4 < " + std::to_string(L.S) + ")");
+          ln("const float4 q = stitch_dev::ld4(" + in_ptr(o) + " + lin4);");
+          ln(f + "[0] = q.x; " + f + "[1] = q.y; " + f + "[2] = q.z; " + f + "[3] = q.w;");
+          if (L.guard) {
+            close();
+            ln("else { " + f + "[0] = " + f + "[1] = " + f + "[2] = " + f + "[3] = 0.0f; }");
+          }
+          close();
+          freevec_[o] = f;
+        }
+      }
       ln("#pragma unroll");
       open("for (int u = 0; u < " + std::to_string(L.vec) + "; ++u)");
       memo_.emplace_back();
@@ -1038,6 +1080,7 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
       memo_.pop_back();
       close();
       close();
+      freevec_.clear();
       for (int g : grp) {
         loop_scalar_.erase(g);
         if (escapes.count(g)) reg_[g] = "r" + std::to_string(g);
@@ -1563,7 +1606,17 @@ KernelSpec Builder::build() {
     for (const Component& c : comps) total_w += c.weight;
     std::vector<std::string> lo(comps.size()), n(comps.size());
     indent_ = 1;
-    if (comps.size() > 1) {
+    if (comps.size() > 1 && opts_.pack_sequential) {
+      // Kernel packing by composition: every CTA runs every component over
+      // its share of that component's rows, one after the other, so the
+      // load balances by construction (no idle CTA ranges at the barrier).
+      ln("// kernel packing: " + std::to_string(comps.size()) + " independent components, each over the whole grid");
+      for (size_t i = 0; i < comps.size(); ++i) {
+        lo[i] = "0";
+        n[i] = "gridDim.x";
+      }
+      spec_.composition.insert("packing");
+    } else if (comps.size() > 1) {
       int64_t cum = 0;
       ln("// kernel packing: " + std::to_string(comps.size()) + " independent components on disjoint CTA ranges");
       std::vector<std::string> bounds;
@@ -1591,6 +1644,9 @@ KernelSpec Builder::build() {
     chunked_ = comps.size() == 1 && comps[0].scheme == "row" && comps[0].cross.empty() && comps[0].post.empty() &&
                comps[0].free_out.empty();
     if (comps.size() == 1 && comps[0].scheme == "row") spec_.rows = comps[0].R;
+    if (comps.size() > 1)
+      for (const Component& c : comps)
+        if (c.scheme == "row") spec_.rows = std::max(spec_.rows, c.R);
     if (chunked_) {
       spec_.chunkable = true;
       spec_.rows_per_cta = comps[0].cta ? 1 : block / 32;
@@ -1598,7 +1654,8 @@ KernelSpec Builder::build() {
     for (size_t i = 0; i < comps.size(); ++i) {
       Component& c = comps[i];
       for (int x : c.cross) cross_parts_[x] = "(int)" + n[i];
-      if (comps.size() > 1) open("if ((int)blockIdx.x >= " + lo[i] + " && (int)blockIdx.x < cb" + std::to_string(i + 1) + ")");
+      const bool ranged = comps.size() > 1 && !opts_.pack_sequential;
+      if (ranged) open("if ((int)blockIdx.x >= " + lo[i] + " && (int)blockIdx.x < cb" + std::to_string(i + 1) + ")");
       memo_.emplace_back();
       if (c.scheme == "row") {
         emit_row(c, lo[i], n[i], "");
@@ -1626,7 +1683,7 @@ KernelSpec Builder::build() {
         spec_.max_grid = std::max<int>(spec_.max_grid, static_cast<int>(std::min<int64_t>(c.max_grid, 1 << 20)));
       }
       memo_.pop_back();
-      if (comps.size() > 1) close();
+      if (ranged) close();
     }
     for (Component* c : rowc)
       if (!c->cross.empty()) smem_floats = std::max<int64_t>(smem_floats, block);
@@ -1670,7 +1727,9 @@ KernelSpec Builder::build() {
   spec_.source = head.str() + body_src + "}\n";
   spec_.block = block;
   spec_.smem_bytes = static_cast<int>(smem_floats * 4 + (smem_floats ? 16 : 0));
-  if (!sectioned && comps.size() == 1 && comps[0].scheme == "row" && !comps[0].cta) {
+  bool all_warp = !sectioned;
+  for (const Component& c : comps) all_warp = all_warp && ((c.scheme == "row" && !c.cta) || c.scheme == "flat");
+  if (all_warp) {
     // every shared-memory term of a warp-row kernel is per warp
     spec_.flex_block = true;
     spec_.smem_per_warp = static_cast<int>((smem_floats * 4 + (block / 32) - 1) / (block / 32));

@@ -206,3 +206,18 @@ def test_gru_double_buffer_and_prefetch_variants():
     ins = orc.random_inputs(g, seed=52)
     ex = assert_parity(g, fused, ins, tma_double_buffer=True, row_prefetch=True)
     assert "tma2" in ex.info["kernels"][0]["scheme"]
+
+
+VARIANTS = [dict(pack_sequential=True), dict(loop_fusion=False), dict(row_prefetch=True),
+            dict(tma_double_buffer=True)]
+
+
+@pytest.mark.parametrize("name", list(W.CONFIGS))
+@pytest.mark.parametrize("variant", VARIANTS, ids=[next(iter(v)) for v in VARIANTS])
+def test_codegen_variants_parity(name, variant):
+    """Every codegen variant (CTA-range packing, per-op loops, row
+    prefetching, double-buffered TMA) stays within the oracle tolerance; the
+    encoder plans here pack the column reduction beside the row groups."""
+    g = W.CONFIGS[name](**W.SMALL[name])
+    fused = rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT)["fused"]
+    assert_parity(g, fused, orc.random_inputs(g, seed=61), **variant)
