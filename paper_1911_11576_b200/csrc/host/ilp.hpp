@@ -33,6 +33,13 @@ struct IlpInstance {
   // conflict pairwise. Supplied by the planner (one clique per graph node);
   // left empty, the solver derives cliques from the pair list.
   std::vector<int> clique_hint;
+  // Optional: for each variable, the graph nodes its pattern covers (dense
+  // node indices). Variables sharing a node conflict. Enables the
+  // fractional node-price bound (an LP-dual bound of the set-packing
+  // relaxation): any feasible selection totals at most
+  // sum_x max_{P covers x} s_P / |P|.
+  std::vector<std::vector<int>> node_sets;
+  int num_nodes = 0;
 };
 
 struct FusionPlan {
