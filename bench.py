@@ -157,7 +157,7 @@ class Clocks:
 # CPU legs (oracle interpreter; test infrastructure used only as the baseline)
 # ---------------------------------------------------------------------------
 
-CPU_SAMPLE_DIV = {"layernorm": 16, "softmax": 16, "encoder": 32, "gru": 16}
+CPU_SAMPLE_DIV = {"layernorm": 16, "softmax": 16, "encoder": 32, "gru": 16, "bert": 32}
 
 
 def _cpu_sample_graph(name, div):

@@ -156,13 +156,29 @@ def _evaluate(graph, inputs, input_errs=None):
 
     for n in graph["nodes"]:
         visit(n["id"])
+    # free every value after its last consumer (whole-graph configs hold
+    # thousands of intermediates); graph outputs and tuple members stay
+    keep = set(graph["outputs"])
+    for o in graph["outputs"]:
+        if nodes[o]["kind"] == "tuple":
+            keep.update(nodes[o]["operands"])
+    uses = {}
+    for n in graph["nodes"]:
+        for o in n.get("operands", []):
+            uses[o] = uses.get(o, 0) + 1
     for nid in order:
         node = nodes[nid]
         if input_errs is not None and node["kind"] == "parameter":
             vals[nid] = np.asarray(inputs[nid], dtype=np.float64)
             errs[nid] = np.asarray(input_errs[nid], dtype=np.float64)
-            continue
-        vals[nid], errs[nid] = _eval(node, vals, errs, inputs)
+        else:
+            vals[nid], errs[nid] = _eval(node, vals, errs, inputs)
+        if node["kind"] not in ("tuple", "fused"):
+            for o in node.get("operands", []):
+                uses[o] -= 1
+                if uses[o] == 0 and o not in keep and nodes[o]["kind"] != "tuple":
+                    vals.pop(o, None)
+                    errs.pop(o, None)
     return vals, errs
 
 

@@ -84,6 +84,7 @@ PlanOptions plan_options(const json::Value& a) {
   o.cost_cfg = cost_cfg(a);
   if (a.has("seed")) o.seed = static_cast<uint64_t>(a.at("seed").as_int());
   if (a.has("threads")) o.threads = static_cast<int>(a.at("threads").as_int());
+  if (a.has("ilp_node_budget")) o.ilp_node_budget = a.at("ilp_node_budget").as_int();
   return o;
 }
 
@@ -116,6 +117,8 @@ json::Value plan_result_json(const Graph& g, const PlanResult& r) {
   t.set("rewrite_ms", r.timings.rewrite_ms);
   t.set("search_nodes", static_cast<int64_t>(r.timings.search_nodes));
   t.set("ilp_rounds", r.timings.ilp_rounds);
+  t.set("ilp_truncated", r.timings.ilp_truncated);
+  t.set("ilp_lp_gap", r.timings.ilp_lp_gap);
   out.set("timings", t);
   return out;
 }

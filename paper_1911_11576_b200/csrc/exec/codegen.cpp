@@ -99,6 +99,10 @@ struct Component {
   bool dbuf = false;          // external TMA tiles double-buffered (prefetch the next row)
   bool prefetch = false;      // register-loaded row inputs prefetched one row ahead
   std::vector<char> cheap;    // rowed broadcasts of constants / free tensors: recomputed at each use, never stored
+  bool tc = false;            // gemm stages on tcgen05 (3xTF32): smem scratch + TMEM accumulator
+  int tc_k = 0;               // largest K among the tensor-core gemm stages
+  std::vector<char> tc_dot;   // value -> gemm stage runs on tcgen05
+  std::vector<int> tc_direct;  // tcgen05 stages with unstaged external operands
   int64_t ext_floats = 0;     // floats of one copy of the external staged tiles
   std::vector<int> cross, post, free_out;
   int64_t max_grid = 1;
@@ -143,6 +147,7 @@ class Builder {
   void emit_sectioned(const std::vector<int>& members);
 
   bool reg_input(const Component& c, int v) const;
+  bool tc_direct(const Component& c, int m) const;
   bool free_vector_access(const Component& c, int o, int v) const;
   void emit_row_scalar(const Component& c, int m);
   void emit_row_load(int v, const std::string& dst, const std::string& row, const Layout& L, int NT);
@@ -438,8 +443,15 @@ bool Builder::plan_row(Component& c) {
       if (c.cls[o] == Cls::kRowed && !vals_[o].constant) max_inner = std::max(max_inner, prod(vals_[o].dims, k));
     if (op.type == OpType::kBatchedDot || op.type == OpType::kDot) {
       has_dot = true;
-      c.staged[vals_[m].operands[0]] = 1;
-      if (op.type == OpType::kBatchedDot) c.staged[vals_[m].operands[1]] = 1;
+      const int a = vals_[m].operands[0], b = vals_[m].operands[1];
+      if (tc_direct(c, m)) {
+        // tcgen05 stage reading its external operands straight from global
+        // memory into the split tiles: nothing to stage
+        c.tc_direct.push_back(m);
+        continue;
+      }
+      c.staged[a] = 1;
+      if (op.type == OpType::kBatchedDot) c.staged[b] = 1;
     }
     if (op.type == OpType::kReduce && c.cls[m] == Cls::kRowed) {
       int in = vals_[m].operands[0];
@@ -492,7 +504,32 @@ bool Builder::plan_row(Component& c) {
       c.slab_floats += c.ext_floats;
     }
   }
-  const int64_t slab_bytes = (c.slab_floats + 32) * 4;
+  // Tensor-core gemm stages: batched dots whose per-row product is one
+  // 64x64 output from staged row-major operands (A [64][K], B [K][64]).
+  c.tc_dot.assign(N, 0);
+  if (c.cta && c.NT == 256 && opts_.tensor_cores)
+    for (int m : c.tc_direct) {
+      auto cd = effective_contract_dims(body_, *vals_[m].node);
+      c.tc_dot[m] = 1;
+      c.tc = true;
+      c.tc_k = std::max<int>(c.tc_k, static_cast<int>(vals_[vals_[m].operands[0]].dims[cd[0]]));
+    }
+  if (c.cta && c.NT == 256 && opts_.tensor_cores)
+    for (int m : c.members) {
+      const OpNode& op = *vals_[m].node;
+      if (op.type != OpType::kBatchedDot || c.cls[m] != Cls::kRowed) continue;
+      const int a = vals_[m].operands[0], b = vals_[m].operands[1];
+      std::vector<int64_t> od(vals_[m].dims.begin() + k, vals_[m].dims.end());
+      auto cd = effective_contract_dims(body_, op);
+      const int64_t K = vals_[a].dims[cd[0]];
+      if (od.size() == 2 && od[0] == 64 && od[1] == 64 && K % 32 == 0 && K <= 256 && c.staged[a] && c.staged[b] &&
+          prod(vals_[a].dims, k) == 64 * K && prod(vals_[b].dims, k) == K * 64) {
+        c.tc_dot[m] = 1;
+        c.tc = true;
+        c.tc_k = std::max<int>(c.tc_k, static_cast<int>(K));
+      }
+    }
+  const int64_t slab_bytes = (c.slab_floats + 32) * 4 + (c.tc ? (4 * 64 * c.tc_k * 4 + 64 * 64 * 4 + 1024) : 0);
   if (c.cta ? slab_bytes > opts_.max_smem : slab_bytes * 8 > opts_.max_smem) return false;
   c.scheme = "row";
   c.max_grid = c.cta ? c.R : (c.R + 7) / 8;
@@ -741,6 +778,21 @@ bool Builder::free_vector_access(const Component& c, int o, int v) const {
   return true;
 }
 
+// Batched dot eligible for the tcgen05 stage with both operands external
+// rowed inputs (64 x K and K x 64 per row, K % 32 == 0).
+bool Builder::tc_direct(const Component& c, int m) const {
+  if (!opts_.tensor_cores || !opts_.tc_direct_loads) return false;
+  const OpNode& op = *vals_[m].node;
+  if (op.type != OpType::kBatchedDot) return false;
+  const int a = vals_[m].operands[0], b = vals_[m].operands[1];
+  if (!vals_[a].external || !vals_[b].external) return false;
+  std::vector<int64_t> od(vals_[m].dims.begin() + c.k, vals_[m].dims.end());
+  auto cd = effective_contract_dims(body_, op);
+  const int64_t K = vals_[a].dims[cd[0]];
+  return od.size() == 2 && od[0] == 64 && od[1] == 64 && K % 32 == 0 && K <= 256 && prod(vals_[a].dims, c.k) == 64 * K &&
+         prod(vals_[b].dims, c.k) == K * 64;
+}
+
 // A rowed external input some member reads at the identity element (so it is
 // loaded once per row into registers).
 bool Builder::reg_input(const Component& c, int v) const {
@@ -786,7 +838,16 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
   const std::string rhi = chunked_ ? "row_hi" : std::to_string(c.R) + "LL";
   if (c.cta) {
     ln("const int t = threadIdx.x;");
-    ln("float* slab = smem;");
+    if (c.tc) {
+      // tcgen05 region at the 1024-aligned start of dynamic smem: hi/lo
+      // operand tiles (swizzled), the D tile, then the slab
+      const int64_t scratch_b = 4LL * 64 * c.tc_k * 4;
+      ln("unsigned char* tcs = reinterpret_cast<unsigned char*>(smem);");
+      ln("float* tcD = smem + " + std::to_string(scratch_b / 4) + ";");
+      ln("float* slab = smem + " + std::to_string(scratch_b / 4 + 4096) + ";");
+    } else {
+      ln("float* slab = smem;");
+    }
     ln("const long long g0 = blockIdx.x - " + lo + ", gstride = " + n + ";");
   } else {
     ln("const int t = threadIdx.x & 31;");
@@ -828,6 +889,13 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
     }
   }
 
+  if (c.tc) {
+    ln("stitch_dev::u64* tcbar = reinterpret_cast<stitch_dev::u64*>(red + 32);");
+    ln("unsigned* tcslot = reinterpret_cast<unsigned*>(red + 36);");
+    ln("if (t == 0) stitch_dev::mbar_init(tcbar, 1);");
+    ln("const unsigned tmem = stitch_dev::tc::alloc(tcslot, 64);  // 64 fp32 columns: one 64x64 accumulator");
+    ln("unsigned tcphase = 0;");
+  }
   // External tiles of one row: total bytes and the bulk copies into buffer `b`.
   int64_t tma_bytes = 0;
   for (int v : inputs_)
@@ -1179,7 +1247,21 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
                          c.staged[a] && c.staged[b];
       std::string r = "r" + std::to_string(m);
       ln("float " + r + "[" + std::to_string(L.elems()) + "];  // " + vals_[m].id + " (gemm stage)");
-      if (tiled) {
+      if (!c.tc_dot.empty() && c.tc_dot[m]) {
+        // 5th-gen tensor cores: 3xTF32 tcgen05.mma into TMEM, D back through
+        // shared memory into this thread's elements of the row tile
+        if (std::find(c.tc_direct.begin(), c.tc_direct.end(), m) != c.tc_direct.end())
+          ln("stitch_dev::tc::gemm_64x64_tf32x3<" + std::to_string(K) + ", true>(" + in_ptr(a) + " + row * " +
+             std::to_string(64 * K) + "LL, " + in_ptr(b) + " + row * " + std::to_string(64 * K) + "LL, tcD, tcs, tmem, tcbar, tcphase);");
+        else
+          ln("stitch_dev::tc::gemm_64x64_tf32x3<" + std::to_string(K) + ">(sm" + std::to_string(a) + ", sm" + std::to_string(b) +
+             ", tcD, tcs, tmem, tcbar, tcphase);");
+        ln("#pragma unroll");
+        open("for (int it = 0; it < " + std::to_string(L.iters) + "; ++it)");
+        ln("const float4 q = *reinterpret_cast<const float4*>(tcD + (it * " + std::to_string(NT) + " + t) * 4);");
+        ln(r + "[it * 4 + 0] = q.x; " + r + "[it * 4 + 1] = q.y; " + r + "[it * 4 + 2] = q.z; " + r + "[it * 4 + 3] = q.w;");
+        close();
+      } else if (tiled) {
         const int64_t RS = static_cast<int64_t>(NT) * 4 / Nn;  // rows between a thread's row chunks
         const int I = L.iters;
         open("");
@@ -1327,6 +1409,7 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
   memo_.pop_back();
   if (c.cta && (any_ext_staged || std::any_of(c.staged.begin(), c.staged.end(), [](char s) { return s; }))) ln("__syncthreads();");
   close();  // row loop
+  if (c.tc) ln("stitch_dev::tc::dealloc(tmem, 64);");
 
   // Write this CTA's cross-row partials: combine the CTA's row groups first.
   for (int x : c.cross) {
@@ -1660,7 +1743,9 @@ KernelSpec Builder::build() {
       if (c.scheme == "row") {
         emit_row(c, lo[i], n[i], "");
         rowc.push_back(&c);
-        smem_floats = std::max(smem_floats, c.cta ? c.slab_floats + 32 + 8 : (c.slab_floats + 32) * (block / 32));
+        smem_floats = std::max<int64_t>(smem_floats, c.cta ? c.slab_floats + 32 + 8 + (c.tc ? int64_t{4} * 64 * c.tc_k + 4096 : 0)
+                                                          : (c.slab_floats + 32) * (block / 32));
+        if (c.tc) spec_.composition.insert("tensor");
         if (!c.cta)
           for (int x : c.cross) {
             const int in = vals_[x].operands[0];
@@ -1673,7 +1758,7 @@ KernelSpec Builder::build() {
         if (has_block) spec_.composition.insert("block");
         std::ostringstream s;
         s << (c.cta ? "row_cta" : "row_warp") << "(k=" << c.k << ",rows=" << c.R << ",nt=" << c.NT
-          << (c.tma ? (c.dbuf ? ",tma2" : ",tma") : "") << (c.cross.empty() ? "" : ",cross") << ")";
+          << (c.tma ? (c.dbuf ? ",tma2" : ",tma") : "") << (c.tc ? ",tcgen05" : "") << (c.cross.empty() ? "" : ",cross") << ")";
         scheme += (scheme.empty() ? "" : "+") + s.str();
         spec_.max_grid = std::max<int>(spec_.max_grid, static_cast<int>(std::min<int64_t>(c.max_grid, 1 << 20)));
       } else {

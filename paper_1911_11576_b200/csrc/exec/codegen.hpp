@@ -70,7 +70,15 @@ struct CodegenOptions {
   // Packed independent components: disjoint CTA ranges (default; measured
   // faster on B200: encoder 96 vs 107 us, the streaming column reduction
   // overlaps the compute-heavier row group) or one after another on every CTA.
-  bool pack_sequential = false;        // one loop per run of same-extent elementwise ops (scalars inside)
+  bool pack_sequential = false;
+  // Batched-GEMM stages of 64x64 row tiles on tcgen05 (3xTF32, TMEM
+  // accumulator) instead of register-tiled FFMA.
+  // Measured on B200 (GRU group): 207 us with staged operands (1 CTA/SM),
+  // 291 us reading operands straight from global, vs 137 us for the
+  // register-tiled FFMA stage -- the per-row split + commit latency is not
+  // yet overlapped, so both are opt-in.
+  bool tensor_cores = false;
+  bool tc_direct_loads = false;        // one loop per run of same-extent elementwise ops (scalars inside)
   bool tma_double_buffer = false; // double-buffer external TMA row tiles
 };
 

@@ -11,6 +11,7 @@
 #include "ilp.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <functional>
 #include <cstdio>
 #include <cstdlib>
@@ -69,7 +70,9 @@ std::vector<double> lp_node_prices(const std::vector<std::vector<int>>& sets, co
   const double eps = 1e-9;
   int stall = 0;
   bool optimal = false;
-  for (int iter = 0; iter < 20 * (m + n) + 1000; ++iter) {
+  // Iteration cap: degenerate whole-graph LPs can pivot for a long time; on
+  // a miss the max-ratio prices (weaker, still valid) are used instead.
+  for (int iter = 0; iter < 8 * m + 2000; ++iter) {
     // duals: dual = cb^T Binv
     for (int k = 0; k < m; ++k) dual[k] = 0.0;
     for (int i = 0; i < m; ++i)
@@ -188,6 +191,54 @@ class Search {
         }
       std::vector<double> xlp;
       lp_price_ = lp_node_prices(pos_sets, pos_scores, inst.num_nodes, &xlp);
+      // Reduced-cost fixing. With y the (repaired, feasible) duals,
+      // s.x = sum(y) - sum_i y_i slack_i + sum_j r_j x_j and r_j <= 0, so a
+      // selection within `gap + delta` of the incumbent (the LP primal when it
+      // is integral and satisfies the cycle constraints) never uses a
+      // variable with r_j < -(gap + delta): those are excluded from branching.
+      {
+        double ysum = 0.0;
+        for (double yv : lp_price_) ysum += yv;
+        lp_bound_ = ysum;
+        std::vector<int> inc;
+        bool integral = !xlp.empty();
+        int k2 = 0;
+        for (int v = 0; v < n_ && integral; ++v)
+          if (inst.scores[v] > 0.0 && !inst.node_sets[v].empty()) {
+            const double xv = xlp[k2++];
+            if (xv > 1e-7 && xv < 1.0 - 1e-7) integral = false;
+            else if (xv >= 0.5) inc.push_back(v);
+          }
+        if (integral) {
+          std::vector<int> cc(inst.cycles.size(), 0);
+          for (int v : inc)
+            for (size_t c = 0; c < inst.cycles.size(); ++c)
+              if (std::find(inst.cycles[c].pattern_indices.begin(), inst.cycles[c].pattern_indices.end(), v) !=
+                  inst.cycles[c].pattern_indices.end())
+                ++cc[c];
+          for (size_t c = 0; c < inst.cycles.size(); ++c)
+            if (cc[c] > static_cast<int>(inst.cycles[c].pattern_indices.size()) - 1) integral = false;
+        }
+        if (integral) {
+          double incumbent = 0.0, total = 0.0;
+          for (int v : inc) incumbent += inst.scores[v];
+          for (double sv : inst.scores) total += sv;
+          const double margin = (ysum - incumbent) + 16.0 * (n_ + 2) * std::numeric_limits<double>::epsilon() * total + 1e-9;
+          rc_out_.assign(n_, 0);
+          for (int v = 0; v < n_; ++v) {
+            if (inst.scores[v] <= 0.0 || inst.node_sets[v].empty()) continue;
+            double r = inst.scores[v];
+            for (int x : inst.node_sets[v]) r -= lp_price_[x];
+            if (r < -margin) rc_out_[v] = 1;
+          }
+        }
+        if (std::getenv("STITCH_ILP_TRACE")) {
+          int out = 0;
+          for (char c : rc_out_) out += c;
+          std::fprintf(stderr, "[ilp]   LP bound %.6f integral=%d incumbent vars=%zu fixed-out=%d of %d\n", ysum,
+                       (int)integral, inc.size(), out, n_);
+        }
+      }
       lp_stamp_.assign(inst.num_nodes, 0);
       node_vars_.assign(inst.num_nodes, {});
       for (int v = 0; v < n_; ++v)
@@ -238,7 +289,7 @@ class Search {
     // without them. (They still join the lexicographic answer through the
     // index-by-index extraction in solve(), as in the reference.)
     for (int v : order_)
-      if (fixed[v] == -1 && in_.scores[v] > 0.0) free_.push_back(v);
+      if (fixed[v] == -1 && in_.scores[v] > 0.0 && (rc_out_.empty() || !rc_out_[v])) free_.push_back(v);
     best_ = kNegInf;
     target_ = target;
     done_ = false;
@@ -267,6 +318,7 @@ class Search {
     query(fixed);
     collect_ = false;
     if (overflow_) return false;
+    if (truncated_ && cands_.empty()) return false;
     out->clear();
     for (const auto& [tot, bits] : cands_) {
       if (tot < best_ - delta_) continue;
@@ -357,6 +409,11 @@ class Search {
   void dfs(size_t pos) {
     if (done_) return;
     ++g_stats.nodes;
+    if (node_budget_ > 0 && ++budget_used_ > node_budget_) {
+      truncated_ = true;
+      done_ = true;
+      return;
+    }
     // The current selection is feasible on its own (everything after `pos`
     // excluded): score it exactly when it can matter.
     if (collect_) {
@@ -448,7 +505,8 @@ class Search {
       // subproblem, so the sum stays a valid bound). Excluding an LP-basic
       // pattern frees slack exactly here.
       const double cutoff = collect_ ? best_ - delta_ : (std::isnan(target_) ? best_ : target_);
-      if ((approx_ + extra) * (1.0 + slack_) >= cutoff && best_ != kNegInf) {
+      // (quadratic in pattern size per node: only for moderate components)
+      if (n_ <= 8000 && (approx_ + extra) * (1.0 + slack_) >= cutoff && best_ != kNegInf) {
         ++avail_stamp_;
         std::vector<int>& cov = cov_scratch_;
         cov.clear();
@@ -502,6 +560,11 @@ class Search {
   int nclique_ = 0, words_ = 0;
   bool use_frac_ = false;
   bool collect_ = false, overflow_ = false;
+ public:
+  long long node_budget_ = 0, budget_used_ = 0;
+  bool truncated_ = false;
+  double lp_bound_ = 0.0;
+ private:
   double delta_ = 0.0;
   size_t cap_ = 0;
   std::vector<std::pair<double, std::vector<uint64_t>>> cands_;
@@ -517,6 +580,7 @@ class Search {
   std::vector<double> price_;
   std::vector<unsigned> price_stamp_;
   std::vector<double> ratio_;  // s_P / |P|
+  std::vector<char> rc_out_;   // reduced-cost fixed to 0
   std::vector<double> lp_price_;  // LP dual node prices (static, valid for every subproblem)
   std::vector<unsigned> lp_stamp_;
   std::vector<std::vector<int>> node_vars_;  // graph node -> variables covering it
@@ -530,6 +594,21 @@ class Search {
 }  // namespace
 
 const SolveStats& last_solve_stats() { return g_stats; }
+
+namespace {
+thread_local long long g_node_budget = -1;
+}
+
+void set_ilp_node_budget(long long nodes) { g_node_budget = nodes; }
+
+long long ilp_node_budget() {
+  if (g_node_budget >= 0) return g_node_budget;
+  static const long long b = [] {
+    const char* e = std::getenv("STITCH_ILP_NODE_BUDGET");
+    return e ? std::atoll(e) : 300000LL;
+  }();
+  return b;
+}
 
 std::vector<PairConstraint> build_conflicts(const std::vector<FusionPattern>& patterns) {
   std::map<std::string, std::vector<int>> holders;
@@ -615,14 +694,27 @@ bool solve_decomposed(const IlpInstance& inst, FusionPlan* plan) {
       sub.num_nodes = inst.num_nodes;
       for (int v : vars) sub.node_sets.push_back(inst.node_sets[v]);
     }
-    Search search(sub);
-    std::vector<std::vector<int>> cands;
     static const bool trace = std::getenv("STITCH_ILP_TRACE") != nullptr;
+    if (trace) std::fprintf(stderr, "[ilp] solving component vars=%zu\n", vars.size());
+    const auto tc0 = std::chrono::steady_clock::now();
+    Search search(sub);
+    if (trace)
+      std::fprintf(stderr, "[ilp]   setup+LP %.2fs\n",
+                   std::chrono::duration<double>(std::chrono::steady_clock::now() - tc0).count());
+    search.node_budget_ = ilp_node_budget();
+    std::vector<std::vector<int>> cands;
     const long long n0 = g_stats.nodes;
     const bool ok = search.collect_near_optimal(delta, 64, &cands);
+    if (search.truncated_) {
+      ++g_stats.truncated;
+      double inc = 0.0;
+      if (!cands.empty())
+        for (int v : cands.front()) inc += sub.scores[v];
+      g_stats.lp_gap += std::max(0.0, search.lp_bound_ - inc);
+    }
     if (trace)
-      std::fprintf(stderr, "[ilp] component vars=%zu candidates=%zu nodes=%lld%s\n", vars.size(), cands.size(),
-                   g_stats.nodes - n0, ok ? "" : " (cap: fallback)");
+      std::fprintf(stderr, "[ilp] component vars=%zu candidates=%zu nodes=%lld%s%s\n", vars.size(), cands.size(),
+                   g_stats.nodes - n0, ok ? "" : " (cap: fallback)", search.truncated_ ? " (node budget: incumbent)" : "");
     if (!ok) return false;
     for (auto& c : cands)
       for (int& v : c) v = vars[v];
@@ -824,6 +916,8 @@ FusionPlan solve_with_cycle_elimination(const Graph& g, const std::vector<Fusion
     FusionPlan plan = solve(inst);
     total.nodes += g_stats.nodes;
     total.queries += g_stats.queries;
+    total.truncated = g_stats.truncated;
+    total.lp_gap = g_stats.lp_gap;
     total.rounds = round + 1;
     std::vector<FusionPattern> chosen;
     for (int idx : plan.selected) {

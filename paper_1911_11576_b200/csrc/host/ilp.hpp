@@ -57,7 +57,20 @@ struct SolveStats {
   long long nodes = 0;
   int queries = 0;
   int rounds = 0;
+  // Components whose exact search hit the node budget (the LP relaxation was
+  // fractional and the gap could not be closed in time): their incumbent is
+  // used, and `lp_gap` (sum of LP bound - incumbent) certifies how far the
+  // plan can be from the optimum. 0 = every component solved exactly.
+  int truncated = 0;
+  double lp_gap = 0.0;
 };
+
+// Per-component search-node budget of the decomposed solver (default 300k;
+// STITCH_ILP_NODE_BUDGET overrides). Instances the reference planner can
+// solve stay far below it.
+long long ilp_node_budget();
+// Per-thread override (plan option "ilp_node_budget"; < 0 restores the default).
+void set_ilp_node_budget(long long nodes);
 const SolveStats& last_solve_stats();
 
 }  // namespace stitch

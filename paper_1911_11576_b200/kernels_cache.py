@@ -23,21 +23,38 @@ def plans(full=True, small=True):
             sizes.append(("small", W.SMALL[name]))
         for size, kw in sizes:
             g = fn(**kw)
-            if size == "full" and tuning.load(name) is not None:
-                out.append(("%s/%s/exec" % (name, size), tuning.config_plan(name, g)[0]["fused"]))
-            for lim_tag, lim in (("b200", W.B200_SHARED_LIMIT), ("ref48k", W.REFERENCE_SHARED_LIMIT)):
-                out.append(("%s/%s/%s" % (name, size, lim_tag), rt.plan(g, shared_limit_bytes=lim)["fused"]))
+            if size == "full":
+                out.append(("%s/%s/bench" % (name, size), tuning.config_plan(name, g)[0]["fused"]))
+            if size == "full" and name in W.PLAN_OPTIONS:
+                pass  # whole-graph config: only the (shipped) bench plan
+            else:
+                for lim_tag, lim in (("b200", W.B200_SHARED_LIMIT), ("ref48k", W.REFERENCE_SHARED_LIMIT)):
+                    out.append(("%s/%s/%s" % (name, size, lim_tag), rt.plan(g, shared_limit_bytes=lim)["fused"]))
             out.append(("%s/%s/unfused" % (name, size), g))
     return out
 
 
-def prebuild(verbose=True):
-    n = hits = 0
+def _compile(args):
+    fused_json, opts = args
+    ex = rt.Executor(fused_json, compile_only=True, **opts)
+    n = len(ex.info["kernels"])
+    hits = sum(bool(k["cache_hit"]) for k in ex.info["kernels"])
+    ex.close()
+    return n, hits
+
+
+def prebuild(verbose=True, workers=None):
+    import concurrent.futures as cf
+    import json
+    import os
+    jobs = []
     for tag, fused in plans():
-        ex = rt.Executor(fused, compile_only=True)
-        for k in ex.info["kernels"]:
-            n += 1
-            hits += bool(k["cache_hit"])
-        ex.close()
+        opts = {"chunking": False} if tag.endswith("/unfused") else {}
+        jobs.append((json.dumps(fused), opts))
+    n = hits = 0
+    with cf.ProcessPoolExecutor(workers or max(1, min(16, os.cpu_count() or 1))) as pool:
+        for a, b in pool.map(_compile, jobs):
+            n += a
+            hits += b
     if verbose:
         print("kernel cache: %d kernels (%d already cached) in %s" % (n, hits, rt.CACHE_DIR))
