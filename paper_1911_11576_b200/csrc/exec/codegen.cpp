@@ -99,6 +99,9 @@ struct Component {
   bool dbuf = false;          // external TMA tiles double-buffered (prefetch the next row)
   bool prefetch = false;      // register-loaded row inputs prefetched one row ahead
   std::vector<char> cheap;    // rowed broadcasts of constants / free tensors: recomputed at each use, never stored
+  // COLRED: a lone column reduction of an external [R][C] tensor
+  int64_t cr_R = 0, cr_C = 0, cr_ncb = 0, cr_nch = 0, cr_rpc = 0;
+  int cr_sync = 0;
   bool tc = false;            // gemm stages on tcgen05 (3xTF32): smem scratch + TMEM accumulator
   int tc_k = 0;               // largest K among the tensor-core gemm stages
   std::vector<char> tc_dot;   // value -> gemm stage runs on tcgen05
@@ -121,6 +124,9 @@ class Builder {
   void collect();
   std::vector<Component> components();
   bool plan_row(Component& c);
+  bool plan_colred(Component& c);
+  void emit_colred(Component& c, const std::string& lo, const std::string& n);
+  int colred_sync_ = 2;  // next free sync word (0..1: grid barrier)
   bool all_elementwise(const Component& c) const;
   Layout layout(int64_t S, int NT) const;
   bool identity_broadcast(int in, int out, int k) const;
@@ -311,6 +317,93 @@ bool Builder::identity_broadcast(int in, int out, int k) const {
   for (size_t i = 0; i < m.size(); ++i)
     if (m[i] != static_cast<int>(i)) return false;
   return true;
+}
+
+// COLRED scheme: out[C] = sum/max over R rows of in[R][C] (in external,
+// reduce_dims a leading prefix). 2-D tiles (128-column block x row chunk)
+// over the grid, float4 streaming loads coalesced along the row, a fixed
+// warp-order CTA sum, per-chunk partials in the workspace, and the last CTA
+// of a column block (atomic arrival counter) combining the chunks in chunk
+// order: deterministic, no grid barrier, no cooperative launch.
+bool Builder::plan_colred(Component& c) {
+  if (!opts_.colred || c.members.size() != 1) return false;
+  const int m = c.members[0];
+  const OpNode& op = *vals_[m].node;
+  if (op.type != OpType::kReduce || !vals_[m].output) return false;
+  const int in = vals_[m].operands[0];
+  if (!vals_[in].external) return false;
+  const auto& d = vals_[in].dims;
+  const int j = static_cast<int>(op.reduce_dims.size());
+  if (j < 1 || j >= static_cast<int>(d.size())) return false;
+  for (int i = 0; i < j; ++i)
+    if (op.reduce_dims[i] != i) return false;
+  c.cr_R = prod(d, 0, j);
+  c.cr_C = prod(d, j);
+  if (c.cr_C % 4 != 0 || c.cr_R < 1) return false;
+  c.cr_ncb = (c.cr_C + 127) / 128;
+  int64_t nch = std::max<int64_t>(1, (static_cast<int64_t>(opts_.num_sms) * 8 + c.cr_ncb - 1) / c.cr_ncb);
+  nch = std::min<int64_t>(nch, std::max<int64_t>(1, (c.cr_R + 15) / 16));
+  c.cr_rpc = (c.cr_R + nch - 1) / nch;
+  c.cr_nch = (c.cr_R + c.cr_rpc - 1) / c.cr_rpc;
+  c.cr_sync = colred_sync_;
+  colred_sync_ += static_cast<int>(c.cr_ncb);
+  c.scheme = "colred";
+  c.max_grid = c.cr_ncb * c.cr_nch;
+  return true;
+}
+
+void Builder::emit_colred(Component& c, const std::string& lo, const std::string& n) {
+  const int m = c.members[0];
+  const OpNode& op = *vals_[m].node;
+  const int in = vals_[m].operands[0];
+  const std::string Op = op.elem_name == "max" ? "stitch_dev::MaxOp" : "stitch_dev::SumOp";
+  const std::string C = std::to_string(c.cr_C) + "LL", NCB = std::to_string(c.cr_ncb), NCH = std::to_string(c.cr_nch);
+  const std::string parts = "(ws + " + std::to_string(ws_off_[m]) + "LL)";
+  open("");
+  ln("// colred: " + vals_[m].id + "[" + std::to_string(c.cr_C) + "] over " + std::to_string(c.cr_R) + " rows; " + NCB +
+     " column blocks x " + NCH + " row chunks of " + std::to_string(c.cr_rpc));
+  ln("const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;");
+  ln("int* last = reinterpret_cast<int*>(smem + nw * 128);");
+  open("for (long long tile = (long long)blockIdx.x - " + lo + "; tile < " + NCB + "LL * " + NCH + "LL; tile += " + n + ")");
+  ln("const int cb = (int)(tile % " + NCB + "), ch = (int)(tile / " + NCB + ");");
+  ln("const long long col = (long long)cb * 128 + lane * 4;");
+  ln("const long long r0 = (long long)ch * " + std::to_string(c.cr_rpc) + "LL;");
+  ln("const long long r1 = r0 + " + std::to_string(c.cr_rpc) + "LL < " + std::to_string(c.cr_R) + "LL ? r0 + " +
+     std::to_string(c.cr_rpc) + "LL : " + std::to_string(c.cr_R) + "LL;");
+  ln("float a0 = " + Op + "::init(), a1 = a0, a2 = a0, a3 = a0;");
+  open("if (col < " + C + ")");
+  ln("#pragma unroll 4");
+  open("for (long long r = r0 + warp; r < r1; r += nw)");
+  ln("const float4 v = stitch_dev::ld4_stream(" + in_ptr(in) + " + r * " + C + " + col);");
+  ln("a0 = " + Op + "::apply(a0, v.x); a1 = " + Op + "::apply(a1, v.y); a2 = " + Op + "::apply(a2, v.z); a3 = " + Op +
+     "::apply(a3, v.w);");
+  close();
+  close();
+  ln("smem[warp * 128 + lane * 4 + 0] = a0; smem[warp * 128 + lane * 4 + 1] = a1;");
+  ln("smem[warp * 128 + lane * 4 + 2] = a2; smem[warp * 128 + lane * 4 + 3] = a3;");
+  ln("__syncthreads();");
+  open("if (threadIdx.x < 128 && (long long)cb * 128 + threadIdx.x < " + C + ")");
+  ln("float a = " + Op + "::init();");
+  ln("for (int w = 0; w < nw; ++w) a = " + Op + "::apply(a, smem[w * 128 + threadIdx.x]);");
+  ln(parts + "[(long long)ch * " + C + " + (long long)cb * 128 + threadIdx.x] = a;");
+  close();
+  ln("__threadfence();");
+  ln("__syncthreads();");
+  ln("if (threadIdx.x == 0) *last = atomicAdd(gsync + " + std::to_string(c.cr_sync) + " + cb, 1u) == " + NCH + "u - 1u;");
+  ln("__syncthreads();");
+  open("if (*last)");
+  ln("__threadfence();");
+  open("if (threadIdx.x < 128 && (long long)cb * 128 + threadIdx.x < " + C + ")");
+  ln("float a = " + Op + "::init();");
+  ln("for (int k = 0; k < " + NCH + "; ++k) a = " + Op + "::apply(a, __ldcg(" + parts + " + (long long)k * " + C +
+     " + (long long)cb * 128 + threadIdx.x));");
+  ln(out_ptr(m) + "[(long long)cb * 128 + threadIdx.x] = a;");
+  close();
+  ln("if (threadIdx.x == 0) atomicExch(gsync + " + std::to_string(c.cr_sync) + " + cb, 0u);");
+  close();
+  ln("__syncthreads();");
+  close();
+  close();
 }
 
 bool Builder::plan_row(Component& c) {
@@ -1630,6 +1723,9 @@ KernelSpec Builder::build() {
   std::vector<Component> comps = components();
   bool sectioned = false;
   for (Component& c : comps) {
+    // COLRED only for a kernel's sole component: packed beside a row group,
+    // the streaming cross-row scheme overlaps better (encoder 96 vs 133 us)
+    if (comps.size() == 1 && plan_colred(c)) continue;
     if (plan_row(c)) continue;
     if (all_elementwise(c)) {
       c.scheme = "flat";
@@ -1682,6 +1778,12 @@ KernelSpec Builder::build() {
           ws_floats_ += (So + 63) / 64 * 64;
           materialized_[x] = "(ws + " + std::to_string(off) + "LL)";
         }
+      }
+    for (Component& c : comps)
+      if (c.scheme == "colred") {
+        const int x = c.members[0];
+        ws_off_[x] = ws_floats_;
+        ws_floats_ += c.cr_nch * ((c.cr_C + 63) / 64 * 64);
       }
     spec_.cooperative = coop;
     // CTA ranges per component, proportional to weight.
@@ -1761,6 +1863,14 @@ KernelSpec Builder::build() {
           << (c.tma ? (c.dbuf ? ",tma2" : ",tma") : "") << (c.tc ? ",tcgen05" : "") << (c.cross.empty() ? "" : ",cross") << ")";
         scheme += (scheme.empty() ? "" : "+") + s.str();
         spec_.max_grid = std::max<int>(spec_.max_grid, static_cast<int>(std::min<int64_t>(c.max_grid, 1 << 20)));
+      } else if (c.scheme == "colred") {
+        emit_colred(c, lo[i], n[i]);
+        spec_.composition.insert("block");
+        smem_floats = std::max<int64_t>(smem_floats, 8 * 128 + 4);
+        std::ostringstream cs;
+        cs << "colred(" << c.cr_ncb << "x" << c.cr_nch << ")";
+        scheme += (scheme.empty() ? "" : "+") + cs.str();
+        spec_.max_grid = std::max<int>(spec_.max_grid, static_cast<int>(std::min<int64_t>(c.max_grid, 1 << 20)));
       } else {
         emit_flat(c, lo[i], n[i]);
         spec_.composition.insert("thread");
@@ -1814,13 +1924,14 @@ KernelSpec Builder::build() {
   spec_.smem_bytes = static_cast<int>(smem_floats * 4 + (smem_floats ? 16 : 0));
   bool all_warp = !sectioned;
   for (const Component& c : comps) all_warp = all_warp && ((c.scheme == "row" && !c.cta) || c.scheme == "flat");
+  // (colred components assume blockDim >= 128 and size smem for 8 warps)
   if (all_warp) {
     // every shared-memory term of a warp-row kernel is per warp
     spec_.flex_block = true;
     spec_.smem_per_warp = static_cast<int>((smem_floats * 4 + (block / 32) - 1) / (block / 32));
   }
   spec_.workspace_floats = ws_floats_;
-  spec_.sync_words = (spec_.cooperative || uses_barrier_) ? 2 : 0;
+  spec_.sync_words = std::max((spec_.cooperative || uses_barrier_) ? 2 : 0, colred_sync_ > 2 ? colred_sync_ : 0);
   if (uses_barrier_) spec_.cooperative = true;
   if (spec_.max_grid < 1) spec_.max_grid = 1;
   return spec_;

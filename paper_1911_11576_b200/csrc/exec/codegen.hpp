@@ -67,6 +67,7 @@ struct CodegenOptions {
   // are opt-in.
   bool row_prefetch = false;      // prefetch the next row's register tiles
   bool loop_fusion = true;
+  bool colred = true;             // dedicated 2-D tiled scheme for lone column reductions
   // Packed independent components: disjoint CTA ranges (default; measured
   // faster on B200: encoder 96 vs 107 us, the streaming column reduction
   // overlaps the compute-heavier row group) or one after another on every CTA.
