@@ -573,30 +573,6 @@ bool Builder::plan_row(Component& c) {
   }
   if (max_inner > static_cast<int64_t>(c.NT) * 64) return false;  // too large for registers
   // shared-memory slab per row group
-  // Slab layout: computed staged values first, then the external (TMA)
-  // tiles; with double buffering a second copy of the external tiles
-  // follows so the next row's loads overlap this row's compute.
-  int64_t off = 0;
-  c.smem_off.assign(N, -1);
-  for (int pass = 0; pass < 2; ++pass)
-    for (int v = 0; v < N; ++v)
-      if (c.staged[v] && vals_[v].external == (pass == 1)) {
-        c.smem_off[v] = off;
-        const int64_t f = (prod(vals_[v].dims, k) + 3) / 4 * 4;
-        off += f;
-        if (pass == 1) c.ext_floats += f;
-      }
-  c.slab_floats = off;
-  if (c.cta) {
-    bool tma_ok = true;
-    for (int v = 0; v < N; ++v)
-      if (c.staged[v] && vals_[v].external) tma_ok = tma_ok && prod(vals_[v].dims, k) % 4 == 0;
-    c.tma = tma_ok && std::any_of(inputs_.begin(), inputs_.end(), [&](int v) { return c.staged[v] != 0; });
-    if (opts_.tma_double_buffer && c.tma && (c.slab_floats + c.ext_floats + 32 + 8) * 4 <= opts_.max_smem) {
-      c.dbuf = true;
-      c.slab_floats += c.ext_floats;
-    }
-  }
   // Tensor-core gemm stages: batched dots whose per-row product is one
   // 64x64 output from staged row-major operands (A [64][K], B [K][64]).
   c.tc_dot.assign(N, 0);
@@ -622,6 +598,31 @@ bool Builder::plan_row(Component& c) {
         c.tc_k = std::max<int>(c.tc_k, static_cast<int>(K));
       }
     }
+  // Slab layout: computed staged values first, then the external (TMA)
+  // tiles; with double buffering a second copy of the external tiles
+  // follows so the next row's loads overlap this row's compute.
+  int64_t off = 0;
+  c.smem_off.assign(N, -1);
+  for (int pass = 0; pass < 2; ++pass)
+    for (int v = 0; v < N; ++v)
+      if (c.staged[v] && vals_[v].external == (pass == 1)) {
+        c.smem_off[v] = off;
+        const int64_t f = (prod(vals_[v].dims, k) + 3) / 4 * 4;
+        off += f;
+        if (pass == 1) c.ext_floats += f;
+      }
+  c.slab_floats = off;
+  if (c.cta) {
+    bool tma_ok = true;
+    for (int v = 0; v < N; ++v)
+      if (c.staged[v] && vals_[v].external) tma_ok = tma_ok && prod(vals_[v].dims, k) % 4 == 0;
+    c.tma = tma_ok && std::any_of(inputs_.begin(), inputs_.end(), [&](int v) { return c.staged[v] != 0; });
+    const int64_t tc_bytes = c.tc ? (4LL * 64 * c.tc_k * 4 + 64 * 64 * 4 + 1024) : 0;
+    if (opts_.tma_double_buffer && c.tma && (c.slab_floats + c.ext_floats + 32 + 8) * 4 + tc_bytes <= opts_.max_smem) {
+      c.dbuf = true;
+      c.slab_floats += c.ext_floats;
+    }
+  }
   const int64_t slab_bytes = (c.slab_floats + 32) * 4 + (c.tc ? (4 * 64 * c.tc_k * 4 + 64 * 64 * 4 + 1024) : 0);
   if (c.cta ? slab_bytes > opts_.max_smem : slab_bytes * 8 > opts_.max_smem) return false;
   c.scheme = "row";
