@@ -60,6 +60,7 @@ int stitch_executor_create(const char* fused_graph_json, const char* options_jso
     if (o.has("tc_direct_loads")) opts.codegen.tc_direct_loads = o.at("tc_direct_loads").as_bool();
     if (o.has("tensor_cores")) opts.codegen.tensor_cores = o.at("tensor_cores").as_bool();
     if (o.has("pack_sequential")) opts.codegen.pack_sequential = o.at("pack_sequential").as_bool();
+    if (o.has("wide_cross_cta")) opts.codegen.wide_cross_cta = o.at("wide_cross_cta").as_bool();
     if (o.has("colred")) opts.codegen.colred = o.at("colred").as_bool();
     if (o.has("loop_fusion")) opts.codegen.loop_fusion = o.at("loop_fusion").as_bool();
     if (o.has("row_prefetch")) opts.codegen.row_prefetch = o.at("row_prefetch").as_bool();

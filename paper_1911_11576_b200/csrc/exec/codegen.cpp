@@ -342,7 +342,9 @@ bool Builder::plan_colred(Component& c) {
   if (c.cr_C % 4 != 0 || c.cr_R < 1) return false;
   c.cr_ncb = (c.cr_C + 127) / 128;
   int64_t nch = std::max<int64_t>(1, (static_cast<int64_t>(opts_.num_sms) * 8 + c.cr_ncb - 1) / c.cr_ncb);
-  nch = std::min<int64_t>(nch, std::max<int64_t>(1, (c.cr_R + 15) / 16));
+  // at least 64 rows per chunk: the last CTA of a column block folds every
+  // chunk, so more chunks lengthen that serial tail
+  nch = std::min<int64_t>(nch, std::max<int64_t>(1, c.cr_R / 64));
   c.cr_rpc = (c.cr_R + nch - 1) / nch;
   c.cr_nch = (c.cr_R + c.cr_rpc - 1) / c.cr_rpc;
   c.cr_sync = colred_sync_;
@@ -393,11 +395,31 @@ void Builder::emit_colred(Component& c, const std::string& lo, const std::string
   ln("__syncthreads();");
   open("if (*last)");
   ln("__threadfence();");
-  open("if (threadIdx.x < 128 && (long long)cb * 128 + threadIdx.x < " + C + ")");
+  // every thread folds a strided slice of the chunks (8 interleaved chains,
+  // fixed order), then slice partials join in slice order
+  ln("const int slices = blockDim.x / 128, sl = threadIdx.x / 128, cc = threadIdx.x % 128;");
   ln("float a = " + Op + "::init();");
-  ln("for (int k = 0; k < " + NCH + "; ++k) a = " + Op + "::apply(a, __ldcg(" + parts + " + (long long)k * " + C +
-     " + (long long)cb * 128 + threadIdx.x));");
-  ln(out_ptr(m) + "[(long long)cb * 128 + threadIdx.x] = a;");
+  open("if (sl < slices && (long long)cb * 128 + cc < " + C + ")");
+  ln("float q[8];");
+  ln("#pragma unroll");
+  ln("for (int u = 0; u < 8; ++u) q[u] = " + Op + "::init();");
+  ln("int k = sl;");
+  open("for (; k + 7 * slices < " + NCH + "; k += 8 * slices)");
+  ln("#pragma unroll");
+  ln("for (int u = 0; u < 8; ++u) q[u] = " + Op + "::apply(q[u], __ldcg(" + parts + " + (long long)(k + u * slices) * " + C +
+     " + (long long)cb * 128 + cc));");
+  close();
+  ln("for (; k < " + NCH + "; k += slices) q[0] = " + Op + "::apply(q[0], __ldcg(" + parts + " + (long long)k * " + C +
+     " + (long long)cb * 128 + cc));");
+  ln("a = " + Op + "::apply(" + Op + "::apply(" + Op + "::apply(q[0], q[1]), " + Op + "::apply(q[2], q[3])), " + Op +
+     "::apply(" + Op + "::apply(q[4], q[5]), " + Op + "::apply(q[6], q[7])));");
+  close();
+  ln("smem[threadIdx.x] = a;");
+  ln("__syncthreads();");
+  open("if (sl == 0 && (long long)cb * 128 + cc < " + C + ")");
+  ln("float v = smem[cc];");
+  ln("for (int j = 1; j < slices; ++j) v = " + Op + "::apply(v, smem[j * 128 + cc]);");
+  ln(out_ptr(m) + "[(long long)cb * 128 + cc] = v;");
   close();
   ln("if (threadIdx.x == 0) atomicExch(gsync + " + std::to_string(c.cr_sync) + " + cb, 0u);");
   close();
@@ -563,10 +585,23 @@ bool Builder::plan_row(Component& c) {
   }
   bool any_staged = std::any_of(c.staged.begin(), c.staged.end(), [](char s) { return s != 0; });
   c.cta = has_dot || any_staged || max_inner > 1024;
+  // Register pressure of a warp-per-row group: every cross-row (column)
+  // reduction keeps max_inner/32 partial sums per lane for the whole row
+  // loop. Wide multi-gradient groups (LayerNorm backward with dgamma / dbeta
+  // / bias gradients: 7 x 24 registers) spill badly, so they go CTA-per-row
+  // where each thread owns max_inner/NT columns.
+  bool wide_cross = false;
+  if (!c.cta && opts_.wide_cross_cta) {
+    int n_cross = 0;
+    for (int m : c.members) n_cross += c.cls[m] == Cls::kCross;
+    wide_cross = n_cross * ((max_inner + 31) / 32) > 48;
+    c.cta = wide_cross;
+  }
   if (c.cta) {
     int nt = 256;
     if (max_inner > 4096) nt = 512;
     if (max_inner > 8192) nt = 1024;
+    if (wide_cross && max_inner % 4 == 0 && (max_inner / 4) % 32 == 0 && max_inner / 4 <= 256) nt = static_cast<int>(max_inner / 4);
     c.NT = nt;
   } else {
     c.NT = 32;
@@ -1740,11 +1775,22 @@ KernelSpec Builder::build() {
   }
 
   // Block size: the widest CTA-mode row component, else 256.
-  int block = 256;
-  for (const Component& c : comps)
+  // (A kernel made only of CTA-row components may use a narrower CTA, e.g.
+  // 192 threads x 4 columns for 768-wide LayerNorm-backward rows; COLRED
+  // needs >= 128 threads; everything else adapts to blockDim.)
+  int block = 0;
+  bool all_cta = true;
+  for (const Component& c : comps) {
     if (c.scheme == "row" && c.cta) block = std::max(block, c.NT);
+    else all_cta = false;
+    if (c.scheme == "colred") block = std::max(block, 256);
+  }
+  if (!all_cta || block == 0) block = std::max(block, 256);
   for (Component& c : comps)
-    if (c.scheme == "row" && c.cta) c.NT = block;
+    if (c.scheme == "row" && c.cta) {
+      if (c.NT != block && c.tc) block = std::max(block, 256);
+      c.NT = block;
+    }
 
   std::ostringstream head;
   std::string body_src;
