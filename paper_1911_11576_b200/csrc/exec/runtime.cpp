@@ -4,6 +4,7 @@
 #include <nvrtc.h>
 
 #include <algorithm>
+#include <numeric>
 #include <cctype>
 #include <cstdio>
 #include <cstring>
@@ -125,6 +126,11 @@ Executor::~Executor() {
   if (!device_ready_) return;
   CudaApi& cu = CudaApi::get();
   if (graph_exec_) cu.cuGraphExecDestroy(static_cast<CUgraphExec>(graph_exec_));
+  for (void* e : in_events_) cu.cuEventDestroy(static_cast<CUevent>(e));
+  for (void* e : kernel_events_) cu.cuEventDestroy(static_cast<CUevent>(e));
+  if (start_event_) cu.cuEventDestroy(static_cast<CUevent>(start_event_));
+  for (void* st : copy_streams_)
+    if (st) cu.cuStreamDestroy(static_cast<CUstream>(st));
   for (void* e : lane_events_) cu.cuEventDestroy(static_cast<CUevent>(e));
   for (void* st : lanes_) cu.cuStreamDestroy(static_cast<CUstream>(st));
   for (KernelInst& k : kernels_)
@@ -585,15 +591,113 @@ void Executor::run_host(const void* const* host_inputs, void* const* host_output
   CUstream s = static_cast<CUstream>(stream);
   std::vector<const void*> din(ni);
   std::vector<void*> dout(no);
-  for (size_t i = 0; i < ni; ++i) {
-    cu_check(cu.cuMemcpyHtoDAsync(host_staging_[i], host_inputs[i], input_bytes_[i], s), "H2D");
-    din[i] = reinterpret_cast<const void*>(host_staging_[i]);
-  }
+  for (size_t i = 0; i < ni; ++i) din[i] = reinterpret_cast<const void*>(host_staging_[i]);
   for (size_t i = 0; i < no; ++i) dout[i] = reinterpret_cast<void*>(host_staging_[ni + i]);
-  run(din.data(), dout.data(), stream);
-  for (size_t i = 0; i < no; ++i)
-    cu_check(cu.cuMemcpyDtoHAsync(host_outputs[i], host_staging_[ni + i], output_bytes_[i], s), "D2H");
+  if (!opts_.overlap_copies || !segments_ok_for_overlap()) {
+    for (size_t i = 0; i < ni; ++i) cu_check(cu.cuMemcpyHtoDAsync(host_staging_[i], host_inputs[i], input_bytes_[i], s), "H2D");
+    run(din.data(), dout.data(), stream);
+    for (size_t i = 0; i < no; ++i)
+      cu_check(cu.cuMemcpyDtoHAsync(host_outputs[i], host_staging_[ni + i], output_bytes_[i], s), "D2H");
+    cu_check(cu.cuStreamSynchronize(s), "stream sync");
+    return;
+  }
+  // Dataflow copy schedule: inputs go up on a copy stream in order of first
+  // use, each kernel waits only for its own inputs, and every output goes
+  // down on a second copy stream as soon as its producing kernel is done --
+  // host->device and device->host transfers overlap each other (full-duplex
+  // link) and the kernels.
+  if (!copy_streams_[0]) {
+    for (int j = 0; j < 2; ++j) {
+      CUstream st;
+      cu_check(cu.cuStreamCreate(&st, CU_STREAM_NON_BLOCKING), "copy stream");
+      copy_streams_[j] = st;
+    }
+    in_events_.resize(ni);
+    for (void*& e : in_events_) {
+      CUevent x;
+      cu_check(cu.cuEventCreate(&x, CU_EVENT_DISABLE_TIMING), "event");
+      e = x;
+    }
+    kernel_events_.resize(kernels_.size());
+    for (void*& e : kernel_events_) {
+      CUevent x;
+      cu_check(cu.cuEventCreate(&x, CU_EVENT_DISABLE_TIMING), "event");
+      e = x;
+    }
+    CUevent x;
+    cu_check(cu.cuEventCreate(&x, CU_EVENT_DISABLE_TIMING), "event");
+    start_event_ = x;
+  }
+  CUstream up = static_cast<CUstream>(copy_streams_[0]), down = static_cast<CUstream>(copy_streams_[1]);
+  cu_check(cu.cuEventRecord(static_cast<CUevent>(start_event_), s), "start");
+  cu_check(cu.cuStreamWaitEvent(up, static_cast<CUevent>(start_event_), 0), "up wait");
+  cu_check(cu.cuStreamWaitEvent(down, static_cast<CUevent>(start_event_), 0), "down wait");
+  // first consumer of every input buffer
+  std::vector<int> first_use(ni, static_cast<int>(kernels_.size()));
+  for (size_t k = 0; k < kernels_.size(); ++k)
+    for (int b : kernels_[k].in_bufs)
+      if (bufs_[b].kind == ValueBuf::kInput) first_use[bufs_[b].slot] = std::min<int>(first_use[bufs_[b].slot], static_cast<int>(k));
+  std::vector<int> order(ni);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return first_use[a] < first_use[b]; });
+  for (int i : order) {
+    cu_check(cu.cuMemcpyHtoDAsync(host_staging_[i], host_inputs[i], input_bytes_[i], up), "H2D");
+    cu_check(cu.cuEventRecord(static_cast<CUevent>(in_events_[i]), up), "in event");
+  }
+  // output slot -> producing kernel
+  std::vector<int> producer(no, -1);
+  for (size_t k = 0; k < kernels_.size(); ++k)
+    for (int b : kernels_[k].out_bufs)
+      if (bufs_[b].kind == ValueBuf::kOutput) producer[bufs_[b].slot] = static_cast<int>(k);
+  std::vector<std::vector<int>> outs_of(kernels_.size());
+  for (size_t o = 0; o < no; ++o)
+    if (producer[o] >= 0) outs_of[producer[o]].push_back(static_cast<int>(o));
+  for (size_t k = 0; k < kernels_.size(); ++k) {
+    for (int b : kernels_[k].in_bufs)
+      if (bufs_[b].kind == ValueBuf::kInput)
+        cu_check(cu.cuStreamWaitEvent(s, static_cast<CUevent>(in_events_[bufs_[b].slot]), 0), "input wait");
+    launch_one(static_cast<int>(k), 0, 1, din.data(), dout.data(), stream);
+    if (outs_of[k].empty()) continue;
+    cu_check(cu.cuEventRecord(static_cast<CUevent>(kernel_events_[k]), s), "kernel event");
+    cu_check(cu.cuStreamWaitEvent(down, static_cast<CUevent>(kernel_events_[k]), 0), "output wait");
+    for (int o : outs_of[k])
+      cu_check(cu.cuMemcpyDtoHAsync(host_outputs[o], host_staging_[ni + o], output_bytes_[o], down), "D2H");
+  }
+  // outputs that alias inputs / other values: copied after everything
+  for (auto [slot, b] : output_copies_) {
+    (void)b;
+    producer[slot] = -2;
+  }
+  bool tail = false;
+  for (size_t o = 0; o < no; ++o) tail = tail || producer[o] < 0;
+  if (tail) {
+    // any output not produced by a kernel directly (aliases): device copy on s, then down
+    for (auto [slot, b] : output_copies_) {
+      const ValueBuf& x = bufs_[b];
+      CUdeviceptr src = x.kind == ValueBuf::kInput ? host_staging_[x.slot]
+                        : x.kind == ValueBuf::kOutput ? host_staging_[ni + x.slot]
+                                                      : arena_ + x.offset;
+      if (x.kind == ValueBuf::kInput)
+        cu_check(cu.cuStreamWaitEvent(s, static_cast<CUevent>(in_events_[x.slot]), 0), "input wait");
+      cu_check(cu.cuMemcpyDtoDAsync(host_staging_[ni + slot], src, output_bytes_[slot], s), "output copy");
+    }
+    CUevent e = static_cast<CUevent>(start_event_);
+    cu_check(cu.cuEventRecord(e, s), "tail event");
+    cu_check(cu.cuStreamWaitEvent(down, e, 0), "tail wait");
+    for (size_t o = 0; o < no; ++o)
+      if (producer[o] < 0) cu_check(cu.cuMemcpyDtoHAsync(host_outputs[o], host_staging_[ni + o], output_bytes_[o], down), "D2H");
+  }
+  cu_check(cu.cuStreamSynchronize(down), "down sync");
   cu_check(cu.cuStreamSynchronize(s), "stream sync");
+  cu_check(cu.cuStreamSynchronize(up), "up sync");
+}
+
+bool Executor::segments_ok_for_overlap() const {
+  // the per-kernel dataflow schedule launches every kernel whole (chunked
+  // schedules keep the plain path)
+  for (const Segment& sg : segments_)
+    if (sg.chunks > 1) return false;
+  return true;
 }
 
 json::Value Executor::profile(const void* const* inputs, void* const* outputs, void* stream, int iters) {

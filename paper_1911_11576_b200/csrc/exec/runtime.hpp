@@ -40,6 +40,9 @@ struct ExecOptions {
   // overlaps kernel j-1's chunk c+1 (tails filled); intermediates use a ring
   // of `chunk_ring` chunk slots.
   bool chunk_pipeline = true;
+  // run_host: dataflow copy schedule (H2D in first-use order on one copy
+  // stream, D2H of each output right after its producer on another)
+  bool overlap_copies = true;
   int chunk_ring = 2;
   CodegenOptions codegen;
 };
@@ -113,6 +116,10 @@ class Executor {
   int launches_per_run_ = 0;
   std::vector<void*> lanes_;        // CUstreams for pipelined chunk lanes
   std::vector<void*> lane_events_;  // CUevents: [segment-local kernel j][chunk c] done, plus fork/join
+  void* copy_streams_[2] = {nullptr, nullptr};  // run_host: H2D and D2H copy streams
+  std::vector<void*> in_events_, kernel_events_;
+  void* start_event_ = nullptr;
+  bool segments_ok_for_overlap() const;
   std::vector<std::string> input_ids_, output_ids_;
   std::vector<int64_t> input_bytes_, output_bytes_;
   std::vector<std::vector<int64_t>> input_dims_, output_dims_;

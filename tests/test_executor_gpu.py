@@ -272,3 +272,23 @@ def test_colred_scheme(R, C):
         _, a = run_device(g, ins)
         _, b = run_device(g, ins)
         assert np.array_equal(a[0], b[0])
+
+
+@pytest.mark.parametrize("name", list(W.CONFIGS))
+def test_run_host_dataflow_copies(name):
+    """stitch_executor_run_host with the dataflow copy schedule (inputs up
+    in first-use order on one copy stream, each output down right after its
+    producer on another) returns exactly what run() computes on device."""
+    g = W.CONFIGS[name](**W.SMALL[name])
+    fused = rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT)["fused"]
+    ins = orc.random_inputs(g, seed=91)
+    ex, ref = run_device(fused, ins)
+    for overlap in (True, False):
+        ex2 = rt.Executor(fused, overlap_copies=overlap)
+        h_in = [torch.from_numpy(ins[i]).pin_memory() for i in ex2.input_ids]
+        h_out = [torch.full(t["dims"], float("nan"), dtype=torch.float32).pin_memory() for t in ex2.info["outputs"]]
+        s = torch.cuda.Stream()
+        for _ in range(2):
+            ex2.run_host(h_in, h_out, stream=s.cuda_stream)
+        for a, b in zip(ref, h_out):
+            assert np.array_equal(a, b.numpy())
