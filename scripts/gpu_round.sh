@@ -14,3 +14,4 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'fusion|dbias' -c 12 \
   -o gpurun_out/prof_full python scripts/profile_configs.py --iters 1 > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
 ls -la gpurun_out
+timeout 900 python bench.py --impl reference --steps 3 --warmup 1 --out gpurun_out/bench_ref.json > gpurun_out/bench_ref.log 2>&1; echo "bench ref rc=$?"
