@@ -118,7 +118,7 @@ class Clocks:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q, "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
 
@@ -297,7 +297,7 @@ def main():
         if not args.no_model_plan and plan_kind.startswith("execution"):
             mplan = rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT)
             model = rt.Executor(mplan["fused"], device=local)
-        base = None if args.no_unfused else rt.Executor(g, device=local, chunking=False)
+        base = None if args.no_unfused else rt.Executor(g, device=local, chunking=False, fold_constants=False)
         ins = [torch.randn(t["dims"], device=dev, generator=gen, dtype=torch.float32) for t in ex.info["inputs"]]
         outs = [torch.empty(t["dims"], device=dev, dtype=torch.float32) for t in ex.info["outputs"]]
         by_id = dict(zip(ex.input_ids, ins))

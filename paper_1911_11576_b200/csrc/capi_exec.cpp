@@ -60,6 +60,7 @@ int stitch_executor_create(const char* fused_graph_json, const char* options_jso
     if (o.has("tc_direct_loads")) opts.codegen.tc_direct_loads = o.at("tc_direct_loads").as_bool();
     if (o.has("tensor_cores")) opts.codegen.tensor_cores = o.at("tensor_cores").as_bool();
     if (o.has("pack_sequential")) opts.codegen.pack_sequential = o.at("pack_sequential").as_bool();
+    if (o.has("wide_cross_threads")) opts.codegen.wide_cross_threads = static_cast<int>(o.at("wide_cross_threads").as_int());
     if (o.has("wide_cross_cta")) opts.codegen.wide_cross_cta = o.at("wide_cross_cta").as_bool();
     if (o.has("colred")) opts.codegen.colred = o.at("colred").as_bool();
     if (o.has("loop_fusion")) opts.codegen.loop_fusion = o.at("loop_fusion").as_bool();
@@ -67,6 +68,7 @@ int stitch_executor_create(const char* fused_graph_json, const char* options_jso
     if (o.has("tma_double_buffer")) opts.codegen.tma_double_buffer = o.at("tma_double_buffer").as_bool();
     if (o.has("chunking")) opts.chunking = o.at("chunking").as_bool();
     if (o.has("chunk_l2_bytes")) opts.chunk_l2_bytes = o.at("chunk_l2_bytes").as_int();
+    if (o.has("fold_constants")) opts.fold_constants = o.at("fold_constants").as_bool();
     if (o.has("overlap_copies")) opts.overlap_copies = o.at("overlap_copies").as_bool();
     if (o.has("chunk_pipeline")) opts.chunk_pipeline = o.at("chunk_pipeline").as_bool();
     if (o.has("chunk_ring")) opts.chunk_ring = static_cast<int>(o.at("chunk_ring").as_int());

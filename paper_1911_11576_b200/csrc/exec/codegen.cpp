@@ -601,7 +601,14 @@ bool Builder::plan_row(Component& c) {
     int nt = 256;
     if (max_inner > 4096) nt = 512;
     if (max_inner > 8192) nt = 1024;
-    if (wide_cross && max_inner % 4 == 0 && (max_inner / 4) % 32 == 0 && max_inner / 4 <= 256) nt = static_cast<int>(max_inner / 4);
+    // wide multi-gradient rows: a small CTA (2 warps for 768 columns) per
+    // row -- ~12 columns per thread, cheap 64-thread barriers, many rows
+    // in flight per SM
+    if (wide_cross) {
+      nt = static_cast<int>(std::min<int64_t>(256, std::max<int64_t>(64, (max_inner / 12 + 31) / 32 * 32)));
+      while (nt > 64 && max_inner % (nt * 4) != 0 && max_inner % nt != 0) nt -= 32;
+      if (opts_.wide_cross_threads > 0) nt = opts_.wide_cross_threads;
+    }
     c.NT = nt;
   } else {
     c.NT = 32;

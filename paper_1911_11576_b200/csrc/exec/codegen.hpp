@@ -71,7 +71,8 @@ struct CodegenOptions {
   // Many column reductions in a wide warp-row group spill registers; CTA per
   // row avoids the spills but serialises 16 barriers per LayerNorm-backward
   // row: measured slower on B200 (BERT LN-backward groups 88 -> 123 us).
-  bool wide_cross_cta = false;             // dedicated 2-D tiled scheme for lone column reductions
+  bool wide_cross_cta = false;
+  int wide_cross_threads = 0;     // CTA size for those rows (0: ~12 columns per thread)             // dedicated 2-D tiled scheme for lone column reductions
   // Packed independent components: disjoint CTA ranges (default; measured
   // faster on B200: encoder 96 vs 107 us, the streaming column reduction
   // overlaps the compute-heavier row group) or one after another on every CTA.

@@ -4,6 +4,7 @@
 #include <nvrtc.h>
 
 #include <algorithm>
+#include <set>
 #include <numeric>
 #include <cctype>
 #include <cstdio>
@@ -168,10 +169,27 @@ void Executor::build_kernels() {
     return static_cast<int>(bufs_.size()) - 1;
   };
 
+  // Uniform constants: value-carrying constants and (unfused) broadcasts of
+  // them. Consumers read them as literals, so a broadcast-of-constant
+  // kernel whose value is not a graph output is dead and never launched.
+  std::map<std::string, double> uniform;
+  std::set<std::string> graph_outs(output_ids_.begin(), output_ids_.end());
+  const std::vector<std::string> topo = topological_sort(g_);
+  for (const std::string& id : topo) {
+    const OpNode& n = g_.at(id);
+    if (n.type == OpType::kConstant && n.value) uniform[id] = *n.value;
+    else if (opts_.fold_constants && n.type == OpType::kElementwise && n.elem_name == "broadcast" &&
+             uniform.count(n.operands.at(0)))
+      uniform[id] = uniform[n.operands[0]];
+  }
   std::map<std::string, std::string> names;
-  for (const std::string& id : topological_sort(g_)) {
+  for (const std::string& id : topo) {
     const OpNode& n = g_.at(id);
     if (n.type != OpType::kFused && !is_fusible(n)) continue;
+    if (n.type != OpType::kFused && uniform.count(id) && !graph_outs.count(id)) {
+      ++folded_kernels_;
+      continue;
+    }
     Graph body;
     std::vector<std::string> outer_inputs;
     std::vector<std::string> out_keys;
@@ -211,8 +229,8 @@ void Executor::build_kernels() {
       if (bn.type != OpType::kParameter) continue;
       const std::string& outer = outer_inputs.at(p++);
       outer_of[bn.id] = outer;
-      const OpNode& on = g_.at(outer);
-      if (on.type == OpType::kConstant && on.value) consts[bn.id] = *on.value;
+      auto u = uniform.find(outer);
+      if (u != uniform.end()) consts[bn.id] = u->second;
     }
     std::string kname = sanitize(id);
     while (names.count(kname)) kname += "_";
@@ -796,6 +814,7 @@ json::Value Executor::describe() const {
   }
   j.set("schedule", sched);
   j.set("launches", launches_per_run_);
+  j.set("folded_constant_kernels", folded_kernels_);
   j.set("algo_bytes", algo);
   j.set("arena_bytes", arena_bytes_);
   j.set("workspace_bytes", ws_floats_ * 4);

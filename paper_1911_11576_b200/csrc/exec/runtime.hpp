@@ -43,6 +43,9 @@ struct ExecOptions {
   // run_host: dataflow copy schedule (H2D in first-use order on one copy
   // stream, D2H of each output right after its producer on another)
   bool overlap_copies = true;
+  // broadcasts of constants left unfused by the plan are folded into their
+  // consumers as literals instead of being materialised by a kernel
+  bool fold_constants = true;
   int chunk_ring = 2;
   CodegenOptions codegen;
 };
@@ -114,6 +117,7 @@ class Executor {
   std::vector<KernelInst> kernels_;
   std::vector<Segment> segments_;
   int launches_per_run_ = 0;
+  int folded_kernels_ = 0;
   std::vector<void*> lanes_;        // CUstreams for pipelined chunk lanes
   std::vector<void*> lane_events_;  // CUevents: [segment-local kernel j][chunk c] done, plus fork/join
   void* copy_streams_[2] = {nullptr, nullptr};  // run_host: H2D and D2H copy streams

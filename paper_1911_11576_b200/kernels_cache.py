@@ -49,7 +49,7 @@ def prebuild(verbose=True, workers=None):
     import os
     jobs = []
     for tag, fused in plans():
-        opts = {"chunking": False} if tag.endswith("/unfused") else {}
+        opts = {"chunking": False, "fold_constants": False} if tag.endswith("/unfused") else {}
         jobs.append((json.dumps(fused), opts))
     n = hits = 0
     with cf.ProcessPoolExecutor(workers or max(1, min(16, os.cpu_count() or 1))) as pool:

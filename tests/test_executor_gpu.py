@@ -292,3 +292,15 @@ def test_run_host_dataflow_copies(name):
             ex2.run_host(h_in, h_out, stream=s.cuda_stream)
         for a, b in zip(ref, h_out):
             assert np.array_equal(a, b.numpy())
+
+
+def test_constant_folding_is_exact():
+    """Unfused broadcasts of constants folded into their consumers as
+    literals give bit-identical results to materialising them."""
+    g = W.layernorm(rows=64, cols=768)
+    ins = orc.random_inputs(g, seed=101)
+    ex_a, a = run_device(g, ins)
+    ex_b, b = run_device(g, ins, fold_constants=False)
+    assert ex_a.info["folded_constant_kernels"] > 0 and ex_b.info["folded_constant_kernels"] == 0
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
