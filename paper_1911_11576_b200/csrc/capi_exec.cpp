@@ -57,6 +57,7 @@ int stitch_executor_create(const char* fused_graph_json, const char* options_jso
     if (o.has("smem_limit_bytes")) opts.codegen.max_smem = static_cast<int>(o.at("smem_limit_bytes").as_int());
     if (o.has("allow_row")) opts.codegen.allow_row = o.at("allow_row").as_bool();
     if (o.has("num_sms")) opts.codegen.num_sms = static_cast<int>(o.at("num_sms").as_int());
+    if (o.has("tc_pipeline")) opts.codegen.tc_pipeline = o.at("tc_pipeline").as_bool();
     if (o.has("tc_direct_loads")) opts.codegen.tc_direct_loads = o.at("tc_direct_loads").as_bool();
     if (o.has("tensor_cores")) opts.codegen.tensor_cores = o.at("tensor_cores").as_bool();
     if (o.has("pack_sequential")) opts.codegen.pack_sequential = o.at("pack_sequential").as_bool();

@@ -106,6 +106,9 @@ struct Component {
   int tc_k = 0;               // largest K among the tensor-core gemm stages
   std::vector<char> tc_dot;   // value -> gemm stage runs on tcgen05
   std::vector<int> tc_direct;  // tcgen05 stages with unstaged external operands
+  bool tcp = false;            // pipelined tcgen05 schedule (next row's MMAs overlap this row's epilogue)
+  std::vector<int> tc_list;    // tcgen05 gemm members in order
+  std::vector<char> tc_raw;    // TMA-staged operand tiles only the tcgen05 split reads
   int64_t ext_floats = 0;     // floats of one copy of the external staged tiles
   std::vector<int> cross, post, free_out;
   int64_t max_grid = 1;
@@ -640,6 +643,30 @@ bool Builder::plan_row(Component& c) {
         c.tc_k = std::max<int>(c.tc_k, static_cast<int>(K));
       }
     }
+  // Pipelined tcgen05 schedule: every staged tile is an external operand of
+  // a tcgen05 stage (so the raw TMA buffer is free once the split ran) and
+  // at most two stages per row (2 rows x 2 accumulators x 64 TMEM columns).
+  c.tc_raw.assign(N, 0);
+  if (c.tc && opts_.tc_pipeline) {
+    bool ok = true;
+    for (int m : c.members)
+      if (c.tc_dot[m]) c.tc_list.push_back(m);
+    for (int v = 0; v < N && ok; ++v) {
+      if (!c.staged[v]) continue;
+      bool tc_operand = false;
+      for (int m : c.tc_list)
+        tc_operand = tc_operand || vals_[m].operands[0] == v || vals_[m].operands[1] == v;
+      ok = vals_[v].external && tc_operand;
+    }
+    ok = ok && !c.tc_list.empty() && c.tc_list.size() <= 2 && c.tc_direct.empty();
+    if (ok) {
+      c.tcp = true;
+      for (int v = 0; v < N; ++v)
+        if (c.staged[v]) c.tc_raw[v] = 1;
+    } else {
+      c.tc_list.clear();
+    }
+  }
   // Slab layout: computed staged values first, then the external (TMA)
   // tiles; with double buffering a second copy of the external tiles
   // follows so the next row's loads overlap this row's compute.
@@ -659,13 +686,14 @@ bool Builder::plan_row(Component& c) {
     for (int v = 0; v < N; ++v)
       if (c.staged[v] && vals_[v].external) tma_ok = tma_ok && prod(vals_[v].dims, k) % 4 == 0;
     c.tma = tma_ok && std::any_of(inputs_.begin(), inputs_.end(), [&](int v) { return c.staged[v] != 0; });
-    const int64_t tc_bytes = c.tc ? (4LL * 64 * c.tc_k * 4 + 64 * 64 * 4 + 1024) : 0;
+    const int64_t tc_bytes = c.tc ? (c.tcp ? static_cast<int64_t>(c.tc_list.size()) : 1) * 4LL * 64 * c.tc_k * 4 + 64 * 68 * 4 + 1024 : 0;
     if (opts_.tma_double_buffer && c.tma && (c.slab_floats + c.ext_floats + 32 + 8) * 4 + tc_bytes <= opts_.max_smem) {
       c.dbuf = true;
       c.slab_floats += c.ext_floats;
     }
   }
-  const int64_t slab_bytes = (c.slab_floats + 32) * 4 + (c.tc ? (4 * 64 * c.tc_k * 4 + 64 * 64 * 4 + 1024) : 0);
+  const int64_t tc_sets = c.tcp ? static_cast<int64_t>(c.tc_list.size()) : 1;
+  const int64_t slab_bytes = (c.slab_floats + 32) * 4 + (c.tc ? tc_sets * 4 * 64 * c.tc_k * 4 + 64 * 68 * 4 + 1024 : 0);
   if (c.cta ? slab_bytes > opts_.max_smem : slab_bytes * 8 > opts_.max_smem) return false;
   c.scheme = "row";
   c.max_grid = c.cta ? c.R : (c.R + 7) / 8;
@@ -845,7 +873,7 @@ std::string Builder::row_access(const Component& c, int o, int v, const std::str
       if (ls != loop_scalar_.end()) return ls->second;
       auto r = reg_.find(o);
       if (r != reg_.end()) return r->second + "[" + e + "]";
-      if (c.staged[o]) return "sm" + std::to_string(o) + "[" + lin + "]";
+      if (c.staged[o] && !(c.tcp && c.tc_raw[o])) return "sm" + std::to_string(o) + "[" + lin + "]";
       if (x.external) return "__ldg(" + in_ptr(o) + " + row * " + std::to_string(So) + "LL + " + lin + ")";
     }
     // Gather through the broadcast map within the row.
@@ -978,9 +1006,10 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
       // tcgen05 region at the 1024-aligned start of dynamic smem: hi/lo
       // operand tiles (swizzled), the D tile, then the slab
       const int64_t scratch_b = 4LL * 64 * c.tc_k * 4;
-      ln("unsigned char* tcs = reinterpret_cast<unsigned char*>(smem);");
-      ln("float* tcD = smem + " + std::to_string(scratch_b / 4) + ";");
-      ln("float* slab = smem + " + std::to_string(scratch_b / 4 + 4096) + ";");
+      const int64_t sets = c.tcp ? static_cast<int64_t>(c.tc_list.size()) : 1;
+      ln("unsigned char* tcs = reinterpret_cast<unsigned char*>(smem);  // " + std::to_string(sets) + " split set(s)");
+      ln("float* tcD = smem + " + std::to_string(sets * scratch_b / 4) + ";  // one padded 64x64 D tile, reused by each stage");
+      ln("float* slab = smem + " + std::to_string(sets * scratch_b / 4 + 64 * 68) + ";");
     } else {
       ln("float* slab = smem;");
     }
@@ -1026,10 +1055,12 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
   }
 
   if (c.tc) {
-    ln("stitch_dev::u64* tcbar = reinterpret_cast<stitch_dev::u64*>(red + 32);");
-    ln("unsigned* tcslot = reinterpret_cast<unsigned*>(red + 36);");
+    ln("stitch_dev::u64* tcbar = reinterpret_cast<stitch_dev::u64*>(red + 36);  // after the TMA barriers at red + 32");
+    ln("unsigned* tcslot = reinterpret_cast<unsigned*>(red + 38);");
     ln("if (t == 0) stitch_dev::mbar_init(tcbar, 1);");
-    ln("const unsigned tmem = stitch_dev::tc::alloc(tcslot, 64);  // 64 fp32 columns: one 64x64 accumulator");
+    const int cols = c.tcp ? (c.tc_list.size() > 1 ? 256 : 128) : 64;
+    ln("const unsigned tmem = stitch_dev::tc::alloc(tcslot, " + std::to_string(cols) +
+       ");  // 64 fp32 columns per 64x64 accumulator" + (c.tcp ? " (x2 rows in flight)" : ""));
     ln("unsigned tcphase = 0;");
   }
   // External tiles of one row: total bytes and the bulk copies into buffer `b`.
@@ -1046,7 +1077,9 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
       }
   };
   if (c.tma) {
-    ln("stitch_dev::u64* bar = reinterpret_cast<stitch_dev::u64*>(smem + " + std::to_string(c.slab_floats + 32) + ");");
+    // TMA barriers right after the reduction scratch `red` (relative to the
+    // slab, which the tcgen05 region may displace)
+    ln("stitch_dev::u64* bar = reinterpret_cast<stitch_dev::u64*>(red + 32);");
     ln(c.dbuf ? "if (t == 0) { stitch_dev::mbar_init(bar, 1); stitch_dev::mbar_init(bar + 1, 1); }"
               : "if (t == 0) stitch_dev::mbar_init(bar, 1);");
     ln("__syncthreads();");
@@ -1057,6 +1090,41 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
       issue_tma(rlo + " + g0", "0");
       close();
     }
+  }
+  // tcp: row r+1's split and MMAs are issued before row r's epilogue, into
+  // the other TMEM buffer; row r+2's tiles stream in meanwhile
+  const int ntc = static_cast<int>(c.tc_list.size());
+  auto tcp_split_issue = [&](const std::string& buf_expr) {
+    for (int j = 0; j < ntc; ++j) {
+      const int m = c.tc_list[j];
+      const int a = vals_[m].operands[0], b = vals_[m].operands[1];
+      ln("stitch_dev::tc::split_operands<" + std::to_string(c.tc_k) + ">(slab + " + std::to_string(c.smem_off[a]) +
+         ", slab + " + std::to_string(c.smem_off[b]) + ", tcs + " + std::to_string(j * 4LL * 64 * c.tc_k * 4) + ");");
+    }
+    ln("stitch_dev::tc::publish_operands();  // also: every thread is done with the raw tiles");
+  };
+  auto tcp_issue = [&](const std::string& buf_expr) {
+    open("if (t == 0)");
+    for (int j = 0; j < ntc; ++j)
+      ln("stitch_dev::tc::issue_tf32x3<" + std::to_string(c.tc_k) + ">(tcs + " + std::to_string(j * 4LL * 64 * c.tc_k * 4) +
+         ", tmem + ((" + buf_expr + ") * " + std::to_string(ntc) + " + " + std::to_string(j) + ") * 64);");
+    ln("stitch_dev::tc::commit(tcbar);");
+    close();
+  };
+  if (c.tcp) {
+    ln("int tb = 0;");
+    open("if (" + rlo + " + g0 < " + rhi + ")");
+    open("if (t == 0)");
+    issue_tma(rlo + " + g0", "0");
+    close();
+    ln("stitch_dev::mbar_wait(bar, phase);");
+    ln("phase ^= 1u;");
+    tcp_split_issue("0");
+    open("if (t == 0 && " + rlo + " + g0 + gstride < " + rhi + ")");
+    issue_tma(rlo + " + g0 + gstride", "0");
+    close();
+    tcp_issue("0");
+    close();
   }
   if (c.prefetch) {
     for (int v : inputs_)
@@ -1080,6 +1148,21 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
   bool any_ext_staged = false;
   for (int v : inputs_)
     if (c.staged[v]) any_ext_staged = true;
+  if (c.tcp) {
+    any_ext_staged = false;  // the tcgen05 pipeline owns the raw tiles
+    ln("stitch_dev::mbar_wait(tcbar, tcphase);  // this row's MMAs are done");
+    ln("tcphase ^= 1u;");
+    ln("stitch_dev::tc::fence_after();");
+    open("if (row + gstride < " + rhi + ")");
+    ln("stitch_dev::mbar_wait(bar, phase);  // next row's tiles landed");
+    ln("phase ^= 1u;");
+    tcp_split_issue("tb ^ 1");
+    open("if (t == 0 && row + 2 * gstride < " + rhi + ")");
+    issue_tma("row + 2 * gstride", "0");
+    close();
+    tcp_issue("tb ^ 1");
+    close();
+  }
   if (any_ext_staged) {
     if (c.dbuf) {
       // prefetch the next row into the other buffer (its readers finished at
@@ -1114,7 +1197,7 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
   // With prefetching (row_pf), the next row's tiles are already in flight in
   // pf<v> while this row computes: the loop renames pf -> r and re-issues.
   for (int v : inputs_) {
-    if (c.cls[v] != Cls::kRowed || c.staged[v]) continue;
+    if (c.cls[v] != Cls::kRowed || (c.staged[v] && !(c.tcp && c.tc_raw[v]))) continue;
     const int64_t S = prod(vals_[v].dims, k);
     if (S == 1) {
       std::string s = fresh("s");
@@ -1383,7 +1466,16 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
                          c.staged[a] && c.staged[b];
       std::string r = "r" + std::to_string(m);
       ln("float " + r + "[" + std::to_string(L.elems()) + "];  // " + vals_[m].id + " (gemm stage)");
-      if (!c.tc_dot.empty() && c.tc_dot[m]) {
+      if (c.tcp && c.tc_dot[m]) {
+        const int j = static_cast<int>(std::find(c.tc_list.begin(), c.tc_list.end(), m) - c.tc_list.begin());
+        ln("stitch_dev::tc::accum_to_smem(tmem + (tb * " + std::to_string(ntc) + " + " + std::to_string(j) + ") * 64, tcD);");
+        ln("#pragma unroll");
+        open("for (int it = 0; it < " + std::to_string(L.iters) + "; ++it)");
+        ln("const int e4 = (it * " + std::to_string(NT) + " + t) * 4;");
+        ln("const float4 q = *reinterpret_cast<const float4*>(tcD + (e4 >> 6) * stitch_dev::tc::kDStride + (e4 & 63));");
+        ln(r + "[it * 4 + 0] = q.x; " + r + "[it * 4 + 1] = q.y; " + r + "[it * 4 + 2] = q.z; " + r + "[it * 4 + 3] = q.w;");
+        close();
+      } else if (!c.tc_dot.empty() && c.tc_dot[m]) {
         // 5th-gen tensor cores: 3xTF32 tcgen05.mma into TMEM, D back through
         // shared memory into this thread's elements of the row tile
         if (std::find(c.tc_direct.begin(), c.tc_direct.end(), m) != c.tc_direct.end())
@@ -1394,7 +1486,8 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
              ", tcD, tcs, tmem, tcbar, tcphase);");
         ln("#pragma unroll");
         open("for (int it = 0; it < " + std::to_string(L.iters) + "; ++it)");
-        ln("const float4 q = *reinterpret_cast<const float4*>(tcD + (it * " + std::to_string(NT) + " + t) * 4);");
+        ln("const int e4 = (it * " + std::to_string(NT) + " + t) * 4;");
+        ln("const float4 q = *reinterpret_cast<const float4*>(tcD + (e4 >> 6) * stitch_dev::tc::kDStride + (e4 & 63));");
         ln(r + "[it * 4 + 0] = q.x; " + r + "[it * 4 + 1] = q.y; " + r + "[it * 4 + 2] = q.z; " + r + "[it * 4 + 3] = q.w;");
         close();
       } else if (tiled) {
@@ -1543,9 +1636,10 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
     close();
   }
   memo_.pop_back();
+  if (c.tcp) ln("tb ^= 1;");
   if (c.cta && (any_ext_staged || std::any_of(c.staged.begin(), c.staged.end(), [](char s) { return s; }))) ln("__syncthreads();");
   close();  // row loop
-  if (c.tc) ln("stitch_dev::tc::dealloc(tmem, 64);");
+  if (c.tc) ln("stitch_dev::tc::dealloc(tmem, " + std::string(c.tcp ? (c.tc_list.size() > 1 ? "256" : "128") : "64") + ");");
 
   // Write this CTA's cross-row partials: combine the CTA's row groups first.
   for (int x : c.cross) {
@@ -1899,7 +1993,10 @@ KernelSpec Builder::build() {
       if (c.scheme == "row") {
         emit_row(c, lo[i], n[i], "");
         rowc.push_back(&c);
-        smem_floats = std::max<int64_t>(smem_floats, c.cta ? c.slab_floats + 32 + 8 + (c.tc ? int64_t{4} * 64 * c.tc_k + 4096 : 0)
+        smem_floats = std::max<int64_t>(smem_floats, c.cta ? c.slab_floats + 32 + 8 +
+                                                                 (c.tc ? (c.tcp ? static_cast<int64_t>(c.tc_list.size()) : 1) *
+                                                                                 int64_t{4} * 64 * c.tc_k + 64 * 68
+                                                                       : 0)
                                                           : (c.slab_floats + 32) * (block / 32));
         if (c.tc) spec_.composition.insert("tensor");
         if (!c.cta)

@@ -84,7 +84,8 @@ struct CodegenOptions {
   // register-tiled FFMA stage -- the per-row split + commit latency is not
   // yet overlapped, so both are opt-in.
   bool tensor_cores = false;
-  bool tc_direct_loads = false;        // one loop per run of same-extent elementwise ops (scalars inside)
+  bool tc_direct_loads = false;
+  bool tc_pipeline = true;        // with tensor_cores: next row's split + MMAs before this row's epilogue        // one loop per run of same-extent elementwise ops (scalars inside)
   bool tma_double_buffer = false; // double-buffer external TMA row tiles
 };
 

@@ -11,16 +11,16 @@ __global__ void __launch_bounds__(256) probe(const float* A, const float* B, flo
   float* sA = reinterpret_cast<float*>(sm);
   float* sB = sA + 4096;
   float* sD = sB + 4096;
-  unsigned char* scratch = sm + 3 * 16384;
-  u64* bar = reinterpret_cast<u64*>(sm + 3 * 16384 + 65536);
-  u32* slot = reinterpret_cast<u32*>(sm + 3 * 16384 + 65536 + 16);
+  unsigned char* scratch = sm + 4 * 16384;
+  u64* bar = reinterpret_cast<u64*>(sm + 4 * 16384 + 65536);
+  u32* slot = reinterpret_cast<u32*>(sm + 4 * 16384 + 65536 + 16);
   if (threadIdx.x == 0) mbar_init(bar, 1);
   const u32 tmem = tc::alloc(slot, 64);
   u32 phase = 0;
   for (int i = threadIdx.x; i < 4096; i += blockDim.x) { sA[i] = A[i]; sB[i] = B[i]; }
   __syncthreads();
   tc::gemm_64x64_tf32x3<64>(sA, sB, sD, scratch, tmem, bar, phase);
-  for (int i = threadIdx.x; i < 4096; i += blockDim.x) D[i] = sD[i];
+  for (int i = threadIdx.x; i < 4096; i += blockDim.x) D[i] = sD[(i / 64) * tc::kDStride + i % 64];
   // raw TMEM dump: warps 0-3, lane quarter w, all 32 lanes, columns 0..63
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (w < 4) {
@@ -49,7 +49,7 @@ int main() {
   float *dA, *dB, *dD, *dR;
   std::vector<float> R(128 * 64);
   cudaMalloc(&dA, 16384); cudaMalloc(&dB, 16384); cudaMalloc(&dD, 16384); cudaMalloc(&dR, 128 * 64 * 4);
-  const int smem = 3 * 16384 + 65536 + 64;
+  const int smem = 4 * 16384 + 65536 + 64;
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   for (int test = 0; test < 2; ++test) {
     cudaMemcpy(dA, test == 0 ? I.data() : V.data(), 16384, cudaMemcpyHostToDevice);

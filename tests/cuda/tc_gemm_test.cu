@@ -14,10 +14,10 @@ __global__ void __launch_bounds__(256) tc_test(const float* A, const float* B, f
   extern __shared__ __align__(1024) unsigned char sm[];
   float* sA = reinterpret_cast<float*>(sm);           // 16 KB
   float* sB = sA + 4096;                              // 16 KB
-  float* sD = sB + 4096;                              // 16 KB
-  unsigned char* scratch = sm + 3 * 16384;            // 64 KB, 1024-aligned
-  u64* bar = reinterpret_cast<u64*>(sm + 3 * 16384 + 65536);
-  u32* slot = reinterpret_cast<u32*>(sm + 3 * 16384 + 65536 + 16);
+  float* sD = sB + 4096;                              // 17 KB (padded rows)
+  unsigned char* scratch = sm + 4 * 16384;            // 64 KB, 1024-aligned
+  u64* bar = reinterpret_cast<u64*>(sm + 4 * 16384 + 65536);
+  u32* slot = reinterpret_cast<u32*>(sm + 4 * 16384 + 65536 + 16);
   if (threadIdx.x == 0) mbar_init(bar, 1);
   const u32 tmem = tc::alloc(slot, 64);
   u32 phase = 0;
@@ -28,7 +28,7 @@ __global__ void __launch_bounds__(256) tc_test(const float* A, const float* B, f
     }
     __syncthreads();
     tc::gemm_64x64_tf32x3<64>(sA, sB, sD, scratch, tmem, bar, phase);
-    for (int i = threadIdx.x; i < 4096; i += blockDim.x) D[(long long)b * 4096 + i] = sD[i];
+    for (int i = threadIdx.x; i < 4096; i += blockDim.x) D[(long long)b * 4096 + i] = sD[(i / 64) * tc::kDStride + i % 64];
     __syncthreads();
   }
   tc::dealloc(tmem, 64);
@@ -45,7 +45,7 @@ int main() {
   cudaMemcpy(dA, A.data(), A.size() * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(dB, B.data(), B.size() * 4, cudaMemcpyHostToDevice);
   cudaMemset(dD, 0xff, D.size() * 4);
-  const int smem = 3 * 16384 + 65536 + 64;
+  const int smem = 4 * 16384 + 65536 + 64;
   cudaFuncSetAttribute(tc_test, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   tc_test<<<148, 256, smem>>>(dA, dB, dD, batch);
   cudaError_t e = cudaDeviceSynchronize();
