@@ -69,6 +69,7 @@ int stitch_executor_create(const char* fused_graph_json, const char* options_jso
     if (o.has("tma_double_buffer")) opts.codegen.tma_double_buffer = o.at("tma_double_buffer").as_bool();
     if (o.has("chunking")) opts.chunking = o.at("chunking").as_bool();
     if (o.has("chunk_l2_bytes")) opts.chunk_l2_bytes = o.at("chunk_l2_bytes").as_int();
+    if (o.has("pdl")) opts.pdl = o.at("pdl").as_bool();
     if (o.has("fold_constants")) opts.fold_constants = o.at("fold_constants").as_bool();
     if (o.has("overlap_copies")) opts.overlap_copies = o.at("overlap_copies").as_bool();
     if (o.has("chunk_pipeline")) opts.chunk_pipeline = o.at("chunk_pipeline").as_bool();

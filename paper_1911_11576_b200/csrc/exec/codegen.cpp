@@ -2069,6 +2069,12 @@ KernelSpec Builder::build() {
   head << "extern \"C\" __global__ void __launch_bounds__(" << block << ") " << name_ << "(" << join(params, ", ")
        << ") {\n";
   head << "  extern __shared__ __align__(128) float smem[];\n";
+  // Programmatic dependent launch: this grid may be scheduled while the
+  // previous kernel drains; wait for it (and its memory) before touching any
+  // global data, and let the next kernel get scheduled right away (our grids
+  // are one resident wave, so its CTAs only take slots this one leaves free).
+  head << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
+  head << "  asm volatile(\"griddepcontrol.launch_dependents;\");\n";
   head << "  (void)ws; (void)gsync; (void)smem; (void)row_lo; (void)row_hi;\n";
   spec_.source = head.str() + body_src + "}\n";
   spec_.block = block;

@@ -508,6 +508,13 @@ void Executor::launch_one(int i, int c, int chunks, const void* const* inputs, v
     attr[0].value.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+  } else if (opts_.pdl) {
+    // overlap this launch with the previous kernel's tail (the kernel waits
+    // in griddepcontrol.wait before reading anything)
+    attr[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+    attr[0].value.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
   }
   cu_check(cu.cuLaunchKernelEx(&cfg, static_cast<CUfunction>(k.fn), args, nullptr), k.spec.name.c_str());
 }

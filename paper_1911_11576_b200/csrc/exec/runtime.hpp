@@ -46,6 +46,8 @@ struct ExecOptions {
   // broadcasts of constants left unfused by the plan are folded into their
   // consumers as literals instead of being materialised by a kernel
   bool fold_constants = true;
+  // programmatic dependent launch between consecutive (non-cooperative) kernels
+  bool pdl = true;
   int chunk_ring = 2;
   CodegenOptions codegen;
 };
