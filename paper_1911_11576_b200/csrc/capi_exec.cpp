@@ -63,6 +63,7 @@ int stitch_executor_create(const char* fused_graph_json, const char* options_jso
     if (o.has("pack_sequential")) opts.codegen.pack_sequential = o.at("pack_sequential").as_bool();
     if (o.has("wide_cross_threads")) opts.codegen.wide_cross_threads = static_cast<int>(o.at("wide_cross_threads").as_int());
     if (o.has("wide_cross_cta")) opts.codegen.wide_cross_cta = o.at("wide_cross_cta").as_bool();
+    if (o.has("lazy_inputs")) opts.codegen.lazy_inputs = o.at("lazy_inputs").as_bool();
     if (o.has("colred")) opts.codegen.colred = o.at("colred").as_bool();
     if (o.has("loop_fusion")) opts.codegen.loop_fusion = o.at("loop_fusion").as_bool();
     if (o.has("row_prefetch")) opts.codegen.row_prefetch = o.at("row_prefetch").as_bool();

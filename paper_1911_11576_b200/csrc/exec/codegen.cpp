@@ -99,6 +99,7 @@ struct Component {
   bool dbuf = false;          // external TMA tiles double-buffered (prefetch the next row)
   bool prefetch = false;      // register-loaded row inputs prefetched one row ahead
   std::vector<char> cheap;    // rowed broadcasts of constants / free tensors: recomputed at each use, never stored
+  std::vector<char> lazy;     // rowed inputs loaded per fused-loop step (float4) instead of preloaded per row
   // COLRED: a lone column reduction of an external [R][C] tensor
   int64_t cr_R = 0, cr_C = 0, cr_ncb = 0, cr_nch = 0, cr_rpc = 0;
   int cr_sync = 0;
@@ -167,6 +168,7 @@ class Builder {
   std::map<int, std::string> reg_;  // value -> register array name (per row body)
   std::map<int, std::string> loop_scalar_;  // value -> scalar of the current fused elementwise loop
   std::map<int, std::string> freevec_;      // free external -> float[4] of the current `it` (fused loop)
+  std::map<int, std::string> rowvec_;       // lazy rowed input -> float[4] of the current `it` (fused loop)
   std::map<int, std::string> scalar_;
 
   const Graph& body_;
@@ -717,6 +719,30 @@ bool Builder::plan_row(Component& c) {
     }
     if (ok && opts_.loop_fusion) c.cheap[m] = 1;
   }
+  // Register relief for many-input rows (LayerNorm backward reads ~15 row
+  // tensors): beyond 64 preloaded elements per thread, inputs that only
+  // elementwise ops read at their own element are loaded inside each fused
+  // loop step (one 128-bit load per 4 elements) instead of for the whole row.
+  c.lazy.assign(N, 0);
+  {
+    int64_t pre = 0;
+    std::vector<int> cand;
+    for (int v : inputs_)
+      if (c.cls[v] == Cls::kRowed && !c.staged[v] && prod(vals_[v].dims, k) > 1 && reg_input(c, v)) {
+        pre += layout(prod(vals_[v].dims, k), c.NT).elems();
+        bool only_ew = true;
+        for (int cns : vals_[v].consumers) {
+          if (std::find(c.members.begin(), c.members.end(), cns) == c.members.end()) continue;
+          const OpNode& co = *vals_[cns].node;
+          only_ew = only_ew && co.type == OpType::kElementwise && c.cls[cns] == Cls::kRowed &&
+                    (co.elem_name != "broadcast" || identity_broadcast(v, cns, k)) &&
+                    prod(vals_[cns].dims, k) == prod(vals_[v].dims, k);
+        }
+        if (only_ew) cand.push_back(v);
+      }
+    if (opts_.lazy_inputs && opts_.loop_fusion && pre > 64 && layout(prod(vals_[cand.empty() ? 0 : cand[0]].dims, k), c.NT).vec == 4)
+      for (int v : cand) c.lazy[v] = 1;
+  }
   // Prefetch the next row's register tiles when the extra registers fit.
   int64_t pf_regs = 0;
   for (int v : inputs_)
@@ -871,6 +897,8 @@ std::string Builder::row_access(const Component& c, int o, int v, const std::str
     if (ident) {
       auto ls = loop_scalar_.find(o);
       if (ls != loop_scalar_.end()) return ls->second;
+      auto rv = rowvec_.find(o);
+      if (rv != rowvec_.end()) return rv->second + "[" + u + "]";
       auto r = reg_.find(o);
       if (r != reg_.end()) return r->second + "[" + e + "]";
       if (c.staged[o] && !(c.tcp && c.tc_raw[o])) return "sm" + std::to_string(o) + "[" + lin + "]";
@@ -1206,6 +1234,7 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
       continue;
     }
     if (!reg_input(c, v)) continue;
+    if (!c.lazy.empty() && c.lazy[v]) continue;  // loaded inside the fused loops
     const Layout L = layout(S, NT);
     const std::string r = "r" + std::to_string(v);
     ln("float " + r + "[" + std::to_string(L.elems()) + "];  // " + vals_[v].id);
@@ -1341,6 +1370,27 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
           close();
           freevec_[o] = f;
         }
+        // lazily loaded row inputs this run reads at its own element
+        std::set<int> lz;
+        for (int g : grp)
+          for (int o : vals_[g].operands)
+            if (!c.lazy.empty() && c.lazy[o] && !reg_.count(o)) lz.insert(o);
+        for (int o : lz) {
+          const std::string f = "rv" + std::to_string(o);
+          const int64_t So = prod(vals_[o].dims, k);
+          ln("float " + f + "[4];");
+          open("");
+          ln("const int lin4 = (it * " + std::to_string(NT) + " + t) * 4;");
+          if (L.guard) open("if (lin4 < " + std::to_string(So) + ")");
+          ln("const float4 q = stitch_dev::ld4(" + in_ptr(o) + " + row * " + std::to_string(So) + "LL + lin4);");
+          ln(f + "[0] = q.x; " + f + "[1] = q.y; " + f + "[2] = q.z; " + f + "[3] = q.w;");
+          if (L.guard) {
+            close();
+            ln("else { " + f + "[0] = " + f + "[1] = " + f + "[2] = " + f + "[3] = 0.0f; }");
+          }
+          close();
+          rowvec_[o] = f;
+        }
       }
       ln("#pragma unroll");
       open("for (int u = 0; u < " + std::to_string(L.vec) + "; ++u)");
@@ -1368,6 +1418,7 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
       close();
       close();
       freevec_.clear();
+      rowvec_.clear();
       for (int g : grp) {
         loop_scalar_.erase(g);
         if (escapes.count(g)) reg_[g] = "r" + std::to_string(g);

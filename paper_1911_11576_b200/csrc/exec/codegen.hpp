@@ -68,6 +68,10 @@ struct CodegenOptions {
   bool row_prefetch = false;      // prefetch the next row's register tiles
   bool loop_fusion = true;
   bool colred = true;
+  // many-input rows: load inputs per fused-loop step, not per row (measured
+  // neutral on the BERT LayerNorm-backward groups: the column-reduction
+  // partials, not the inputs, hold most of the registers)
+  bool lazy_inputs = false;
   // Many column reductions in a wide warp-row group spill registers; CTA per
   // row avoids the spills but serialises 16 barriers per LayerNorm-backward
   // row: measured slower on B200 (BERT LN-backward groups 88 -> 123 us).

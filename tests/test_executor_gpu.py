@@ -213,7 +213,8 @@ def test_gru_double_buffer_and_prefetch_variants():
 
 
 VARIANTS = [dict(pack_sequential=True), dict(loop_fusion=False), dict(row_prefetch=True),
-            dict(tma_double_buffer=True), dict(tensor_cores=True), dict(colred=False)]
+            dict(tma_double_buffer=True), dict(tensor_cores=True), dict(colred=False), dict(lazy_inputs=True),
+            dict(pdl=False), dict(fold_constants=False)]
 
 
 @pytest.mark.parametrize("name", list(W.CONFIGS))
@@ -305,3 +306,10 @@ def test_constant_folding_is_exact():
     assert ex_a.info["folded_constant_kernels"] > 0 and ex_b.info["folded_constant_kernels"] == 0
     for x, y in zip(a, b):
         assert np.array_equal(x, y)
+
+
+def test_bert_lazy_inputs_variant():
+    """Lazily loaded row inputs (opt-in) on the many-input BERT groups."""
+    g = W.bert(batch=2, layers=1)
+    fused = rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT)["fused"]
+    assert_parity(g, fused, orc.random_inputs(g, seed=111, scale=0.5), lazy_inputs=True)
