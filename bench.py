@@ -103,24 +103,47 @@ def ncu_traffic(kernel_name, config):
         return None
 
 
-class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+_SAMPLER = r"""
+import sys, time, pynvml
+pynvml.nvmlInit()
+h = pynvml.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+print("max", pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM), flush=True)
+while True:
+    print(time.monotonic(), pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+          pynvml.nvmlDeviceGetCurrentClocksEventReasons(h), flush=True)
+    time.sleep(0.002)
+"""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+class Clocks:
+    """SM clock and clock-event reasons sampled DURING the timed region
+    (B200_PROFILING.md clocks line): a separate NVML sampler process polls
+    every 2 ms (no GIL contention with the launching thread; nvidia-smi's
+    loop is too coarse for a ~100 ms region); only samples whose timestamps
+    fall inside [mark_start, mark_stop] (CLOCK_MONOTONIC) are kept."""
+
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
 
     def __init__(self, index):
         self.index = index
         self.proc = None
+        self.t0 = self.t1 = None
+        self.max_mhz = 0.0
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q, "--format=csv,noheader,nounits",
-                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.proc = subprocess.Popen([sys.executable, "-c", _SAMPLER, str(self.index)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            first = self.proc.stdout.readline().split()  # "max <MHz>": sampling runs
+            self.max_mhz = float(first[1]) if len(first) == 2 and first[0] == "max" else 0.0
         except Exception:
             self.proc = None
+
+    def mark_start(self):
+        self.t0 = time.monotonic()
+
+    def mark_stop(self):
+        self.t1 = time.monotonic()
 
     def stop(self):
         if self.proc is None:
@@ -131,26 +154,26 @@ class Clocks:
         except Exception:
             self.proc.kill()
             out, _ = self.proc.communicate()
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, reasons, mx = [], set(), self.max_mhz
         for line in out.splitlines():
-            f = [x.strip() for x in line.split(",")]
-            if len(f) < 9:
+            f = line.split()
+            if f and f[0] == "max":
+                mx = float(f[1])
                 continue
             try:
-                s, m = float(f[1]), float(f[2])
-            except ValueError:
+                t, c, r = float(f[0]), float(f[1]), int(f[2])
+            except (ValueError, IndexError):
                 continue
-            sm.append(s)
-            mx = max(mx, m)
-            for n, v in zip(names, f[5:9]):
-                if v.lower() == "active":
+            if self.t0 is not None and not (self.t0 <= t <= (self.t1 or t)):
+                continue
+            sm.append(c)
+            for n, bit in self.REASONS.items():
+                if r & bit:
                     reasons.add(n)
         if not sm:
             return None
-        load = sorted(sm)[len(sm) // 2:] if len(sm) > 2 else sm
-        return {"sm_mhz": float(np.median(load)), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm),
+                "source": "nvml sampler process, 2 ms"}
 
 
 # ---------------------------------------------------------------------------
@@ -338,6 +361,8 @@ def main():
     def measure(which, steps, warmup, clocks=None):
         evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in cfgs]
                for _ in range(steps)]
+        if clocks:
+            clocks.start()
         for _ in range(warmup):
             timed_pass(which, [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                                for _ in cfgs])
@@ -346,13 +371,15 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
         if clocks:
-            clocks.start()
+            clocks.mark_start()
         for s in range(steps):
             timed_pass(which, evs[s])
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
+        if clocks:
+            clocks.mark_stop()
         ck = clocks.stop() if clocks else None
         per_cfg = np.zeros(len(cfgs))
         for s in range(steps):
