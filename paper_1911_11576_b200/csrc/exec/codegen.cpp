@@ -1451,7 +1451,24 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
       const std::string Op = op.elem_name == "max" ? "stitch_dev::MaxOp" : "stitch_dev::SumOp";
       const int64_t Sin = prod(vals_[in].dims, k);
       const Layout Li = layout(Sin, NT);
-      if (S == 1) {
+      if (S == 1 && Sin == 1) {
+        // a reduce over a single element per row is the element itself
+        int src = in;
+        while (c.cls[src] == Cls::kRowed && !c.cheap.empty() && c.cheap[src]) src = vals_[src].operands[0];
+        std::string x;
+        auto sc = scalar_.find(src);
+        auto r = reg_.find(src);
+        if (vals_[src].constant) x = flit(vals_[src].cval);
+        else if (sc != scalar_.end()) x = sc->second;
+        else if (r != reg_.end()) x = r->second + "[0]";
+        else if (c.staged[src]) x = "sm" + std::to_string(src) + "[0]";
+        else if (c.cls[src] == Cls::kRowed && vals_[src].external) x = "__ldg(" + in_ptr(src) + " + row)";
+        else if (c.cls[src] != Cls::kRowed) x = at(src, std::vector<std::string>(vals_[src].dims.size(), "0"));
+        else throw InternalError("row reduce input not in registers: " + vals_[in].id);
+        std::string s = fresh("s");
+        ln("const float " + s + " = " + x + ";  // " + vals_[m].id + " (one element)");
+        scalar_[m] = s;
+      } else if (S == 1) {
         std::string acc = fresh("a");
         ln("float " + acc + " = " + Op + "::init();");
         ln("#pragma unroll");
@@ -2088,6 +2105,7 @@ KernelSpec Builder::build() {
     emit_row_finalize(rowc);
     memo_.pop_back();
     spec_.max_grid = std::max<int>(spec_.max_grid, static_cast<int>(comps.size()));
+    if (comps.size() > 1 && !opts_.pack_sequential) spec_.min_grid = static_cast<int>(comps.size());
     spec_.scheme = scheme;
     body_src = out_.str();
   }

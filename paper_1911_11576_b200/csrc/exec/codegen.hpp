@@ -52,6 +52,7 @@ struct KernelSpec {
   // Warp-per-row kernels read blockDim at run time, so the runtime may launch
   // them with any warp count <= block; shared memory scales per warp.
   bool flex_block = false;
+  int min_grid = 1;                  // ranged packing: at least one CTA per component
   int smem_per_warp = 0;
   int64_t rows = 0;
   int rows_per_cta = 1;

@@ -433,7 +433,11 @@ void Executor::init_device() {
     int64_t useful = std::max(1, k.spec.max_grid);
     if (k.spec.flex_block && k.spec.rows > 0) useful = (k.spec.rows + k.block / 32 - 1) / (k.block / 32);
     if (k.spec.flex_block && k.spec.rows == 0) useful = static_cast<int64_t>(k.spec.max_grid) * k.spec.block / k.block;
+    useful = std::max<int64_t>(useful, k.spec.min_grid);
     k.grid = static_cast<int>(std::min<int64_t>(useful, resident));
+    if (k.grid < k.spec.min_grid)
+      throw std::runtime_error("kernel " + k.spec.name + ": packed components need " + std::to_string(k.spec.min_grid) +
+                               " resident CTAs");
     if (k.spec.cooperative) k.grid = static_cast<int>(std::min<int64_t>(k.grid, static_cast<int64_t>(sms_) * 32));
   }
   cubins_tmp_.clear();

@@ -313,3 +313,21 @@ def test_bert_lazy_inputs_variant():
     g = W.bert(batch=2, layers=1)
     fused = rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT)["fused"]
     assert_parity(g, fused, orc.random_inputs(g, seed=111, scale=0.5), lazy_inputs=True)
+
+
+@pytest.mark.parametrize("seed", range(64))
+def test_random_dag_parity(seed):
+    """Seeded random graphs (elementwise chains, row and column reductions,
+    broadcasts back; tests/helpers.random_dag) through the reference-exact
+    planner at both shared limits, the unfused graph and the SECTIONED
+    fallback: every stitched kernel scheme the generator can pick on shapes
+    it was not tuned for."""
+    from helpers import random_dag
+    R = [3, 64, 100, 257, 1024, 1, 2, 4096][seed % 8]
+    C = [4, 33, 256, 768, 1000, 1, 2, 2048][(seed // 8) % 8]
+    g = random_dag(seed, n_ops=6 + seed % 10, dims=(R, C))
+    ins = orc.random_inputs(g, seed=seed, scale=0.5)
+    for lim in (W.B200_SHARED_LIMIT, W.REFERENCE_SHARED_LIMIT):
+        assert_parity(g, rt.plan(g, shared_limit_bytes=lim)["fused"], ins)
+    assert_parity(g, g, ins)
+    assert_parity(g, rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT)["fused"], ins, allow_row=False)
