@@ -65,6 +65,10 @@ int stitch_executor_create(const char* fused_graph_json, const char* options_jso
     if (o.has("wide_cross_cta")) opts.codegen.wide_cross_cta = o.at("wide_cross_cta").as_bool();
     if (o.has("lazy_inputs")) opts.codegen.lazy_inputs = o.at("lazy_inputs").as_bool();
     if (o.has("colred")) opts.codegen.colred = o.at("colred").as_bool();
+    if (o.has("colred_fused")) opts.codegen.colred_fused = o.at("colred_fused").as_bool();
+    if (o.has("colred_cp_async")) opts.codegen.colred_cp_async = o.at("colred_cp_async").as_bool();
+    if (o.has("colred_cols")) opts.codegen.colred_cols = static_cast<int>(o.at("colred_cols").as_int());
+    if (o.has("colred_ctas_per_sm")) opts.codegen.colred_ctas_per_sm = static_cast<int>(o.at("colred_ctas_per_sm").as_int());
     if (o.has("loop_fusion")) opts.codegen.loop_fusion = o.at("loop_fusion").as_bool();
     if (o.has("row_prefetch")) opts.codegen.row_prefetch = o.at("row_prefetch").as_bool();
     if (o.has("tma_double_buffer")) opts.codegen.tma_double_buffer = o.at("tma_double_buffer").as_bool();

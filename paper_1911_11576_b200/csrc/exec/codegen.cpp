@@ -102,7 +102,7 @@ struct Component {
   std::vector<char> lazy;     // rowed inputs loaded per fused-loop step (float4) instead of preloaded per row
   // COLRED: a lone column reduction of an external [R][C] tensor
   int64_t cr_R = 0, cr_C = 0, cr_ncb = 0, cr_nch = 0, cr_rpc = 0;
-  int cr_sync = 0;
+  int cr_sync = 0, cr_m = -1, cr_w = 128;
   bool tc = false;            // gemm stages on tcgen05 (3xTF32): smem scratch + TMEM accumulator
   int tc_k = 0;               // largest K among the tensor-core gemm stages
   std::vector<char> tc_dot;   // value -> gemm stage runs on tcgen05
@@ -324,33 +324,58 @@ bool Builder::identity_broadcast(int in, int out, int k) const {
   return true;
 }
 
-// COLRED scheme: out[C] = sum/max over R rows of in[R][C] (in external,
-// reduce_dims a leading prefix). 2-D tiles (128-column block x row chunk)
-// over the grid, float4 streaming loads coalesced along the row, a fixed
-// warp-order CTA sum, per-chunk partials in the workspace, and the last CTA
-// of a column block (atomic arrival counter) combining the chunks in chunk
-// order: deterministic, no grid barrier, no cooperative launch.
+// COLRED scheme: out[C] = sum/max over R rows of f(in...)[R][C], where f is
+// the component's elementwise producer chain evaluated inline (LayerNorm
+// dgamma = sum(dy * xhat), a bias gradient = sum(dy)); reduce_dims a leading
+// prefix, the reduce the component's only output. 2-D tiles (128-column
+// block x row chunk) over one wave of CTAs, float4 streaming loads of the
+// same-shape inputs coalesced along the row, a fixed warp-order CTA sum,
+// per-chunk partials in the workspace, and the last CTA of a column block
+// (atomic arrival counter) combining the chunks in chunk order:
+// deterministic, no grid barrier, no cooperative launch.
+// COLRED shared layout (floats): warp partials + flag, then the cp.async
+// stage of kColredStageSlots float4 per thread (256 threads)
+constexpr int kColredStageOff = 8 * 128 + 16;
+constexpr int kColredStageSlots = 8;
+
 bool Builder::plan_colred(Component& c) {
-  if (!opts_.colred || c.members.size() != 1) return false;
-  const int m = c.members[0];
+  if (!opts_.colred) return false;
+  int m = -1;
+  for (int x : c.members) {
+    const OpNode& xo = *vals_[x].node;
+    if (xo.type == OpType::kReduce) {
+      if (m >= 0) return false;
+      m = x;
+    } else if (xo.type != OpType::kElementwise || vals_[x].output) {
+      return false;
+    }
+  }
+  if (m < 0 || !vals_[m].output) return false;
+  if (c.members.size() > 1 && !opts_.colred_fused) return false;
   const OpNode& op = *vals_[m].node;
-  if (op.type != OpType::kReduce || !vals_[m].output) return false;
   const int in = vals_[m].operands[0];
-  if (!vals_[in].external) return false;
+  if (!vals_[in].external && !vals_[in].member) return false;
   const auto& d = vals_[in].dims;
   const int j = static_cast<int>(op.reduce_dims.size());
   if (j < 1 || j >= static_cast<int>(d.size())) return false;
   for (int i = 0; i < j; ++i)
     if (op.reduce_dims[i] != i) return false;
+  c.cr_m = m;
   c.cr_R = prod(d, 0, j);
   c.cr_C = prod(d, j);
   if (c.cr_C % 4 != 0 || c.cr_R < 1) return false;
-  c.cr_ncb = (c.cr_C + 127) / 128;
-  int64_t nch = std::max<int64_t>(1, (static_cast<int64_t>(opts_.num_sms) * 8 + c.cr_ncb - 1) / c.cr_ncb);
-  // at least 64 rows per chunk: the last CTA of a column block folds every
-  // chunk, so more chunks lengthen that serial tail
-  nch = std::min<int64_t>(nch, std::max<int64_t>(1, c.cr_R / 64));
-  c.cr_rpc = (c.cr_R + nch - 1) / nch;
+  // W-column blocks (colred_cols: 32, 64 or 128): a warp load covers
+  // 128 / W * 4 rows x W floats; the last CTA of a block folds W columns
+  const int W = opts_.colred_cols == 32 || opts_.colred_cols == 64 ? opts_.colred_cols : 128;
+  c.cr_w = W;
+  c.cr_ncb = (c.cr_C + W - 1) / W;
+  // one wave of colred_ctas_per_sm CTAs of 8 warps per SM
+  int64_t nch = std::max<int64_t>(1, (static_cast<int64_t>(opts_.num_sms) * opts_.colred_ctas_per_sm) / c.cr_ncb);
+  // at least one full pass of the CTA's row groups per chunk
+  const int64_t pass = 8 * (128 / W);
+  nch = std::min<int64_t>(nch, std::max<int64_t>(1, c.cr_R / pass));
+  // chunks of whole passes: every pass but the matrix's last is unpredicated
+  c.cr_rpc = ((c.cr_R + nch - 1) / nch + pass - 1) / pass * pass;
   c.cr_nch = (c.cr_R + c.cr_rpc - 1) / c.cr_rpc;
   c.cr_sync = colred_sync_;
   colred_sync_ += static_cast<int>(c.cr_ncb);
@@ -360,39 +385,127 @@ bool Builder::plan_colred(Component& c) {
 }
 
 void Builder::emit_colred(Component& c, const std::string& lo, const std::string& n) {
-  const int m = c.members[0];
+  const int m = c.cr_m;
   const OpNode& op = *vals_[m].node;
   const int in = vals_[m].operands[0];
   const std::string Op = op.elem_name == "max" ? "stitch_dev::MaxOp" : "stitch_dev::SumOp";
   const std::string C = std::to_string(c.cr_C) + "LL", NCB = std::to_string(c.cr_ncb), NCH = std::to_string(c.cr_nch);
+  const int W = c.cr_w, LPR = W / 4, G = 32 / LPR;  // lanes per row, rows per warp load
+  const std::string Ws = std::to_string(W);
   const std::string parts = "(ws + " + std::to_string(ws_off_[m]) + "LL)";
+  int64_t iters = std::min<int64_t>(8, c.cr_rpc / (8 * G));  // loads per thread per pass (8-warp CTA)
+  const std::string Gs = std::to_string(G);
   open("");
   ln("// colred: " + vals_[m].id + "[" + std::to_string(c.cr_C) + "] over " + std::to_string(c.cr_R) + " rows; " + NCB +
-     " column blocks x " + NCH + " row chunks of " + std::to_string(c.cr_rpc));
+     " column blocks of " + Ws + " x " + NCH + " row chunks of " + std::to_string(c.cr_rpc));
   ln("const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;");
-  ln("int* last = reinterpret_cast<int*>(smem + nw * 128);");
+  ln("const int sub = lane / " + std::to_string(LPR) + ", cl = lane % " + std::to_string(LPR) + ";");
+  ln("int* last = reinterpret_cast<int*>(smem + " + std::to_string(kColredStageOff - 8) + ");  // past every partial row");
   open("for (long long tile = (long long)blockIdx.x - " + lo + "; tile < " + NCB + "LL * " + NCH + "LL; tile += " + n + ")");
   ln("const int cb = (int)(tile % " + NCB + "), ch = (int)(tile / " + NCB + ");");
-  ln("const long long col = (long long)cb * 128 + lane * 4;");
+  ln("const long long col = (long long)cb * " + Ws + " + cl * 4;");
   ln("const long long r0 = (long long)ch * " + std::to_string(c.cr_rpc) + "LL;");
   ln("const long long r1 = r0 + " + std::to_string(c.cr_rpc) + "LL < " + std::to_string(c.cr_R) + "LL ? r0 + " +
      std::to_string(c.cr_rpc) + "LL : " + std::to_string(c.cr_R) + "LL;");
   ln("float a0 = " + Op + "::init(), a1 = a0, a2 = a0, a3 = a0;");
+  // f(...) at (r, col + u): same-shape external inputs as one float4 each,
+  // then the producer chain inline (broadcast vectors through L1)
+  const auto& d = vals_[in].dims;
+  const int j = static_cast<int>(op.reduce_dims.size());
+  std::vector<int64_t> rd(d.begin(), d.begin() + j), cd(d.begin() + j, d.end());
+  std::set<int> ins, seen;
+  std::function<void(int)> walk = [&](int v) {
+    if (!seen.insert(v).second) return;
+    if (vals_[v].external && vals_[v].dims == d) ins.insert(v);
+    if (vals_[v].member && vals_[v].node->type == OpType::kElementwise && vals_[v].node->elem_name != "broadcast")
+      for (int o : vals_[v].operands) walk(o);
+  };
+  walk(in);
+  if (opts_.colred_cp_async)
+    iters = std::max<int64_t>(1, std::min<int64_t>(iters, kColredStageSlots / std::max<int64_t>(1, static_cast<int64_t>(ins.size()))));
+  const std::string IT = std::to_string(iters);
+  // staging: with colred_cp_async every load of a pass goes through
+  // cp.async into this thread's shared slots (ptxas otherwise keeps only
+  // ~2 rows of float4 loads in flight per thread)
+  const bool cpa = opts_.colred_cp_async;
+  const int nin = static_cast<int>(ins.size());
+  auto body = [&](bool guarded) {
+    std::map<int, std::string> qname;
+    int vi = 0;
+    std::map<int, int> slot;
+    for (int v : ins) {
+      slot[v] = vi++;
+      qname[v] = fresh("q");
+      if (!cpa) ln("float4 " + qname[v] + "[" + IT + "];");
+    }
+    ln("#pragma unroll");
+    open("for (int i = 0; i < " + IT + "; ++i)");
+    ln("const long long r = rb + (i * nw + warp) * " + Gs + " + sub;");
+    for (int v : ins) {
+      const std::string src = in_ptr(v) + " + " + (guarded ? "(r < r1 ? r : r0)" : "r") + " * " + C + " + col";
+      if (cpa)
+        ln("stitch_dev::cp_async16(cstage + (i * " + std::to_string(nin) + " + " + std::to_string(slot[v]) + ") * blockDim.x, " + src +
+           ", " + (guarded ? "r < r1" : "true") + ");");
+      else
+        ln(qname[v] + "[i] = " + (guarded ? "r < r1 ? " : "") + "stitch_dev::ld4_stream(" + src + ")" +
+           (guarded ? " : make_float4(0.f, 0.f, 0.f, 0.f)" : "") + ";");
+    }
+    close();
+    if (cpa) ln("stitch_dev::cp_async_wait_all();");
+    ln("#pragma unroll");
+    open("for (int i = 0; i < " + IT + "; ++i)");
+    ln("const long long r = rb + (i * nw + warp) * " + Gs + " + sub;");
+    if (guarded) open("if (r < r1)");
+    for (int v : ins)
+      if (cpa) ln("const float4 " + qname[v] + " = cstage[(i * " + std::to_string(nin) + " + " + std::to_string(slot[v]) + ") * blockDim.x];");
+    memo_.emplace_back();
+    std::vector<std::string> rc = decode("r", rd);
+    auto coords = [&](int u) {
+      std::vector<std::string> cc = rc;
+      std::vector<std::string> k2 = decode(u ? "(col + " + std::to_string(u) + ")" : std::string("col"), cd);
+      cc.insert(cc.end(), k2.begin(), k2.end());
+      return cc;
+    };
+    const char* lanes[4] = {".x", ".y", ".z", ".w"};
+    for (int v : ins)
+      for (int u = 0; u < 4; ++u)
+        memo_.back()[std::to_string(v) + "@" + join(coords(u), ",")] = qname[v] + (cpa ? "" : "[i]") + lanes[u];
+    std::vector<std::string> xv;
+    for (int u = 0; u < 4; ++u) xv.push_back(at(in, coords(u)));
+    memo_.pop_back();
+    ln("a0 = " + Op + "::apply(a0, " + xv[0] + "); a1 = " + Op + "::apply(a1, " + xv[1] + "); a2 = " + Op + "::apply(a2, " +
+       xv[2] + "); a3 = " + Op + "::apply(a3, " + xv[3] + ");");
+    if (guarded) close();
+    close();
+  };
+  if (cpa) ln("float4* cstage = reinterpret_cast<float4*>(smem + " + std::to_string(kColredStageOff) + ") + threadIdx.x;");
   open("if (col < " + C + ")");
-  ln("#pragma unroll 4");
-  open("for (long long r = r0 + warp; r < r1; r += nw)");
-  ln("const float4 v = stitch_dev::ld4_stream(" + in_ptr(in) + " + r * " + C + " + col);");
-  ln("a0 = " + Op + "::apply(a0, v.x); a1 = " + Op + "::apply(a1, v.y); a2 = " + Op + "::apply(a2, v.z); a3 = " + Op +
-     "::apply(a3, v.w);");
+  open("for (long long rb = r0; rb < r1; rb += " + IT + " * nw * " + Gs + ")");
+  // full passes without predicates (predicate registers would otherwise
+  // serialise the loads), the ragged last pass guarded
+  open("if (rb + " + IT + " * nw * " + Gs + " <= r1)");
+  body(false);
+  close();
+  open("else");
+  body(true);
   close();
   close();
-  ln("smem[warp * 128 + lane * 4 + 0] = a0; smem[warp * 128 + lane * 4 + 1] = a1;");
-  ln("smem[warp * 128 + lane * 4 + 2] = a2; smem[warp * 128 + lane * 4 + 3] = a3;");
+  close();
+  // the warp's row groups, then the CTA's warps in warp order
+  for (int x = LPR; x < 32; x *= 2)
+    for (int u = 0; u < 4; ++u) {
+      const std::string a = "a" + std::to_string(u);
+      ln(a + " = " + Op + "::apply(" + a + ", __shfl_xor_sync(0xffffffffu, " + a + ", " + std::to_string(x) + "));");
+    }
+  ln("if (sub == 0) { smem[warp * " + Ws + " + cl * 4 + 0] = a0; smem[warp * " + Ws + " + cl * 4 + 1] = a1; smem[warp * " + Ws +
+     " + cl * 4 + 2] = a2; smem[warp * " + Ws + " + cl * 4 + 3] = a3; }");
   ln("__syncthreads();");
-  open("if (threadIdx.x < 128 && (long long)cb * 128 + threadIdx.x < " + C + ")");
+  open("for (int i = threadIdx.x; i < " + Ws + "; i += blockDim.x)");
+  open("if ((long long)cb * " + Ws + " + i < " + C + ")");
   ln("float a = " + Op + "::init();");
-  ln("for (int w = 0; w < nw; ++w) a = " + Op + "::apply(a, smem[w * 128 + threadIdx.x]);");
-  ln(parts + "[(long long)ch * " + C + " + (long long)cb * 128 + threadIdx.x] = a;");
+  ln("for (int w = 0; w < nw; ++w) a = " + Op + "::apply(a, smem[w * " + Ws + " + i]);");
+  ln(parts + "[(long long)ch * " + C + " + (long long)cb * " + Ws + " + i] = a;");
+  close();
   close();
   ln("__threadfence();");
   ln("__syncthreads();");
@@ -400,32 +513,68 @@ void Builder::emit_colred(Component& c, const std::string& lo, const std::string
   ln("__syncthreads();");
   open("if (*last)");
   ln("__threadfence();");
-  // every thread folds a strided slice of the chunks (8 interleaved chains,
-  // fixed order), then slice partials join in slice order
-  ln("const int slices = blockDim.x / 128, sl = threadIdx.x / 128, cc = threadIdx.x % 128;");
-  ln("float a = " + Op + "::init();");
-  open("if (sl < slices && (long long)cb * 128 + cc < " + C + ")");
-  ln("float q[8];");
-  ln("#pragma unroll");
-  ln("for (int u = 0; u < 8; ++u) q[u] = " + Op + "::init();");
-  ln("int k = sl;");
-  open("for (; k + 7 * slices < " + NCH + "; k += 8 * slices)");
-  ln("#pragma unroll");
-  ln("for (int u = 0; u < 8; ++u) q[u] = " + Op + "::apply(q[u], __ldcg(" + parts + " + (long long)(k + u * slices) * " + C +
-     " + (long long)cb * 128 + cc));");
-  close();
-  ln("for (; k < " + NCH + "; k += slices) q[0] = " + Op + "::apply(q[0], __ldcg(" + parts + " + (long long)k * " + C +
-     " + (long long)cb * 128 + cc));");
-  ln("a = " + Op + "::apply(" + Op + "::apply(" + Op + "::apply(q[0], q[1]), " + Op + "::apply(q[2], q[3])), " + Op +
-     "::apply(" + Op + "::apply(q[4], q[5]), " + Op + "::apply(q[6], q[7])));");
-  close();
-  ln("smem[threadIdx.x] = a;");
-  ln("__syncthreads();");
-  open("if (sl == 0 && (long long)cb * 128 + cc < " + C + ")");
-  ln("float v = smem[cc];");
-  ln("for (int j = 1; j < slices; ++j) v = " + Op + "::apply(v, smem[j * 128 + cc]);");
-  ln(out_ptr(m) + "[(long long)cb * 128 + cc] = v;");
-  close();
+  if (cpa) {
+    // float4 column groups x strided chunk slices; each round puts
+    // kColredStageSlots partial rows per thread in flight through cp.async,
+    // chunks fold in ascending order per slice, slices join in slice order
+    const std::string S = std::to_string(kColredStageSlots), LG = std::to_string(LPR);
+    ln("const int slices = blockDim.x / " + LG + ", sl = threadIdx.x / " + LG + ", cg = threadIdx.x % " + LG + ";");
+    ln("const long long fcol = (long long)cb * " + Ws + " + cg * 4;");
+    ln("float f0 = " + Op + "::init(), f1 = f0, f2 = f0, f3 = f0;");
+    open("for (int k0 = sl; k0 < " + NCH + "; k0 += slices * " + S + ")");
+    ln("#pragma unroll");
+    open("for (int i = 0; i < " + S + "; ++i)");
+    ln("const int k = k0 + i * slices;");
+    ln("const bool ok = k < " + NCH + " && fcol < " + C + ";");
+    ln("stitch_dev::cp_async16(cstage + i * blockDim.x, " + parts + " + (ok ? (long long)k * " + C + " + fcol : 0LL), ok);");
+    close();
+    ln("stitch_dev::cp_async_wait_all();");
+    ln("#pragma unroll");
+    open("for (int i = 0; i < " + S + "; ++i)");
+    open("if (k0 + i * slices < " + NCH + ")");
+    ln("const float4 p = cstage[i * blockDim.x];");
+    ln("f0 = " + Op + "::apply(f0, p.x); f1 = " + Op + "::apply(f1, p.y); f2 = " + Op + "::apply(f2, p.z); f3 = " + Op + "::apply(f3, p.w);");
+    close();
+    close();
+    close();
+    ln("smem[sl * " + Ws + " + cg * 4 + 0] = f0; smem[sl * " + Ws + " + cg * 4 + 1] = f1; smem[sl * " + Ws + " + cg * 4 + 2] = f2; smem[sl * " +
+       Ws + " + cg * 4 + 3] = f3;");
+    ln("__syncthreads();");
+    open("for (int i = threadIdx.x; i < " + Ws + "; i += blockDim.x)");
+    open("if ((long long)cb * " + Ws + " + i < " + C + ")");
+    ln("float v = smem[i];");
+    ln("for (int j = 1; j < slices; ++j) v = " + Op + "::apply(v, smem[j * " + Ws + " + i]);");
+    ln(out_ptr(m) + "[(long long)cb * " + Ws + " + i] = v;");
+    close();
+    close();
+  } else {
+    // every slice of W threads folds a strided set of the chunks (4
+    // interleaved chains, fixed order), then slice partials join in slice order
+    ln("const int slices = blockDim.x / " + Ws + ", sl = threadIdx.x / " + Ws + ", cc = threadIdx.x % " + Ws + ";");
+    ln("float a = " + Op + "::init();");
+    open("if ((long long)cb * " + Ws + " + cc < " + C + ")");
+    ln("float q[4];");
+    ln("#pragma unroll");
+    ln("for (int u = 0; u < 4; ++u) q[u] = " + Op + "::init();");
+    ln("int k = sl;");
+    open("for (; k + 3 * slices < " + NCH + "; k += 4 * slices)");
+    ln("#pragma unroll");
+    ln("for (int u = 0; u < 4; ++u) q[u] = " + Op + "::apply(q[u], __ldcg(" + parts + " + (long long)(k + u * slices) * " + C +
+       " + (long long)cb * " + Ws + " + cc));");
+    close();
+    ln("for (; k < " + NCH + "; k += slices) q[0] = " + Op + "::apply(q[0], __ldcg(" + parts + " + (long long)k * " + C +
+       " + (long long)cb * " + Ws + " + cc));");
+    ln("a = " + Op + "::apply(" + Op + "::apply(q[0], q[1]), " + Op + "::apply(q[2], q[3]));");
+    close();
+    ln("smem[threadIdx.x] = a;");
+    ln("__syncthreads();");
+    open("if (sl == 0 && (long long)cb * " + Ws + " + cc < " + C + ")");
+    ln("float v = smem[cc];");
+    ln("for (int j = 1; j < slices; ++j) v = " + Op + "::apply(v, smem[j * " + Ws + " + cc]);");
+    ln(out_ptr(m) + "[(long long)cb * " + Ws + " + cc] = v;");
+    close();
+
+  }
   ln("if (threadIdx.x == 0) atomicExch(gsync + " + std::to_string(c.cr_sync) + " + cb, 0u);");
   close();
   ln("__syncthreads();");
@@ -1997,7 +2146,7 @@ KernelSpec Builder::build() {
       }
     for (Component& c : comps)
       if (c.scheme == "colred") {
-        const int x = c.members[0];
+        const int x = c.cr_m;
         ws_off_[x] = ws_floats_;
         ws_floats_ += c.cr_nch * ((c.cr_C + 63) / 64 * 64);
       }
@@ -2085,9 +2234,9 @@ KernelSpec Builder::build() {
       } else if (c.scheme == "colred") {
         emit_colred(c, lo[i], n[i]);
         spec_.composition.insert("block");
-        smem_floats = std::max<int64_t>(smem_floats, 8 * 128 + 4);
+        smem_floats = std::max<int64_t>(smem_floats, opts_.colred_cp_async ? kColredStageOff + 256 * 4 * kColredStageSlots : kColredStageOff);
         std::ostringstream cs;
-        cs << "colred(" << c.cr_ncb << "x" << c.cr_nch << ")";
+        cs << "colred(" << c.cr_ncb << "x" << c.cr_nch << ",w" << c.cr_w << ")";
         scheme += (scheme.empty() ? "" : "+") + cs.str();
         spec_.max_grid = std::max<int>(spec_.max_grid, static_cast<int>(std::min<int64_t>(c.max_grid, 1 << 20)));
       } else {

@@ -69,6 +69,10 @@ struct CodegenOptions {
   bool row_prefetch = false;      // prefetch the next row's register tiles
   bool loop_fusion = true;
   bool colred = true;
+  bool colred_fused = true;
+  int colred_ctas_per_sm = 4;  // COLRED tiles per SM (one resident wave)
+  int colred_cols = 128;       // COLRED column-block width: 32, 64 or 128 floats
+  bool colred_cp_async = true;  // COLRED loads staged through cp.async (all of a pass in flight)  // COLRED also for reduces of an inline elementwise producer chain
   // many-input rows: load inputs per fused-loop step, not per row (measured
   // neutral on the BERT LayerNorm-backward groups: the column-reduction
   // partials, not the inputs, hold most of the registers)

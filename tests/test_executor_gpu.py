@@ -214,7 +214,7 @@ def test_gru_double_buffer_and_prefetch_variants():
 
 VARIANTS = [dict(pack_sequential=True), dict(loop_fusion=False), dict(row_prefetch=True),
             dict(tma_double_buffer=True), dict(tensor_cores=True), dict(colred=False), dict(lazy_inputs=True),
-            dict(pdl=False), dict(fold_constants=False)]
+            dict(pdl=False), dict(fold_constants=False), dict(colred_cp_async=False), dict(colred_cols=32)]
 
 
 @pytest.mark.parametrize("name", list(W.CONFIGS))
@@ -274,6 +274,35 @@ def test_colred_scheme(R, C):
         _, a = run_device(g, ins)
         _, b = run_device(g, ins)
         assert np.array_equal(a[0], b[0])
+
+
+@pytest.mark.parametrize("R,C", [(1, 4), (5, 12), (64, 768), (4096, 768), (1000, 2304), (33, 132)])
+@pytest.mark.parametrize("opts", [{}, {"colred_cols": 32}, {"colred_cols": 64}, {"colred_cp_async": False},
+                                  {"colred_ctas_per_sm": 1}], ids=["w128", "w32", "w64", "ldg", "cta1"])
+def test_colred_fused_producer(R, C, opts):
+    """COLRED with an inline elementwise producer (LayerNorm dgamma =
+    sum_rows(dy * xhat) with a broadcast scale) across column-block widths,
+    cp.async staging or plain loads, and ragged row chunks: within the
+    oracle bound and bit-identical across runs."""
+    g = {"nodes": [{"id": "dy", "kind": "parameter", "shape": {"dims": [R, C], "dtype": "f32"}},
+                   {"id": "xh", "kind": "parameter", "shape": {"dims": [R, C], "dtype": "f32"}},
+                   {"id": "s", "kind": "parameter", "shape": {"dims": [C], "dtype": "f32"}},
+                   {"id": "sb", "kind": "elementwise", "name": "broadcast", "operands": ["s"],
+                    "shape": {"dims": [R, C], "dtype": "f32"}},
+                   {"id": "p", "kind": "elementwise", "name": "multiply", "operands": ["dy", "xh"],
+                    "shape": {"dims": [R, C], "dtype": "f32"}},
+                   {"id": "q", "kind": "elementwise", "name": "multiply", "operands": ["p", "sb"],
+                    "shape": {"dims": [R, C], "dtype": "f32"}},
+                   {"id": "r", "kind": "reduce", "operands": ["q"], "reduce_dims": [0],
+                    "shape": {"dims": [C], "dtype": "f32"}}],
+         "outputs": ["r"]}
+    fused = rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT)["fused"]
+    ins = orc.random_inputs(g, seed=R * 7 + C)
+    ex = assert_parity(g, fused, ins, **opts)
+    assert len(ex.info["kernels"]) == 1 and "colred" in ex.info["kernels"][0]["scheme"]
+    _, a = run_device(fused, ins, **opts)
+    _, b = run_device(fused, ins, **opts)
+    assert np.array_equal(a[0], b[0])
 
 
 @pytest.mark.parametrize("name", list(W.CONFIGS))
