@@ -94,6 +94,7 @@ struct Component {
   std::vector<Cls> cls;
   std::vector<char> staged;
   std::vector<int64_t> smem_off;  // floats within the row-group slab
+  std::map<int, int64_t> cross_off;  // cross_smem: per-warp column accumulators within the slab
   int64_t slab_floats = 0;
   bool tma = false;
   bool dbuf = false;          // external TMA tiles double-buffered (prefetch the next row)
@@ -831,6 +832,28 @@ bool Builder::plan_row(Component& c) {
         off += f;
         if (pass == 1) c.ext_floats += f;
       }
+  // Register relief for warp rows with many column reductions (BERT
+  // LayerNorm-backward groups carry 5-9 [768] parameter gradients, 24
+  // registers each per lane): with cross_smem the per-warp column partials
+  // live in the warp's slab instead of registers when 8 warps still fit.
+  c.cross_off.clear();
+  if (opts_.cross_smem && !c.cta) {
+    int64_t regs = 0, extra = 0;
+    for (int x : c.cross) {
+      const int in = vals_[x].operands[0];
+      if (vals_[x].node->reduce_dims.size() == vals_[in].dims.size()) continue;  // scalar: one register
+      const int64_t S = prod(vals_[in].dims, k);
+      regs += layout(S, 32).elems();
+      extra += (S + 3) / 4 * 4;
+    }
+    if (regs > 48 && (off + extra + 32) * 4 * 8 <= opts_.max_smem)
+      for (int x : c.cross) {
+        const int in = vals_[x].operands[0];
+        if (vals_[x].node->reduce_dims.size() == vals_[in].dims.size()) continue;
+        c.cross_off[x] = off;
+        off += (prod(vals_[in].dims, k) + 3) / 4 * 4;
+      }
+  }
   c.slab_floats = off;
   if (c.cta) {
     bool tma_ok = true;
@@ -856,7 +879,10 @@ bool Builder::plan_row(Component& c) {
     const OpNode& op = *vals_[m].node;
     if (c.cls[m] != Cls::kRowed || op.type != OpType::kElementwise || op.elem_name != "broadcast") continue;
     const int in = vals_[m].operands[0];
-    if (!(vals_[in].constant || c.cls[in] == Cls::kFree)) continue;
+    // (also broadcasts of row scalars -- rstd, mean: the scalar is in a
+    // register already, so the [row] -> [row, C] broadcast costs nothing)
+    if (!(vals_[in].constant || c.cls[in] == Cls::kFree || (c.cls[in] == Cls::kRowed && prod(vals_[in].dims, k) == 1)))
+      continue;
     if (vals_[m].output || c.staged[m] || prod(vals_[m].dims, k) == 1) continue;
     bool ok = true;
     for (int cns : vals_[m].consumers) {
@@ -1224,7 +1250,17 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
     const std::string Op = op.elem_name == "max" ? "stitch_dev::MaxOp" : "stitch_dev::SumOp";
     if (scalar)
       ln("float p" + std::to_string(x) + " = " + Op + "::init();  // " + vals_[x].id);
-    else {
+    else if (c.cross_off.count(x)) {
+      ln("float* p" + std::to_string(x) + " = slab + " + std::to_string(c.cross_off[x]) + ";  // " + vals_[x].id + " (warp partials in shared memory)");
+      ln("#pragma unroll");
+      open("for (int it = 0; it < " + std::to_string(L.iters) + "; ++it)");
+      ln("#pragma unroll");
+      open("for (int u = 0; u < " + std::to_string(L.vec) + "; ++u)");
+      ln("const int lin = (it * " + std::to_string(NT) + " + t) * " + std::to_string(L.vec) + " + u;");
+      ln((L.guard ? "if (lin < " + std::to_string(L.S) + ") " : std::string()) + "p" + std::to_string(x) + "[lin] = " + Op + "::init();");
+      close();
+      close();
+    } else {
       ln("float p" + std::to_string(x) + "[" + std::to_string(L.elems()) + "];  // " + vals_[x].id);
       ln("#pragma unroll");
       ln("for (int e = 0; e < " + std::to_string(L.elems()) + "; ++e) p" + std::to_string(x) + "[e] = " + Op + "::init();");
@@ -1824,7 +1860,8 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
     else if (c.staged[in]) src = "sm" + std::to_string(in) + "[lin]";
     else if (scalar_.count(in)) src = scalar_[in];
     else throw InternalError("cross-row reduce input unavailable: " + vals_[in].id);
-    std::string tgt = scalar ? "p" + std::to_string(x) : "p" + std::to_string(x) + "[it * " + std::to_string(L.vec) + " + u]";
+    std::string tgt = scalar ? "p" + std::to_string(x)
+                             : "p" + std::to_string(x) + (c.cross_off.count(x) ? "[lin]" : "[it * " + std::to_string(L.vec) + " + u]");
     ln((L.guard ? "if (lin < " + std::to_string(L.S) + ") " : std::string()) + tgt + " = " + Op + "::apply(" + tgt + ", " + src + ");");
     close();
     close();
@@ -1887,6 +1924,16 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
       ln((L.guard ? "if (lin < " + std::to_string(So) + ") " : std::string()) + parts + "[" + rank + " * " + std::to_string(So) + "LL + lin] = p" + std::to_string(x) + "[it * " + std::to_string(L.vec) + " + u];");
       close();
       close();
+    } else if (c.cross_off.count(x)) {
+      // the warps' partial rows already sit in their slabs: fixed-order CTA sum
+      ln("__syncthreads();");
+      open("for (int i = threadIdx.x; i < " + std::to_string(So) + "; i += blockDim.x)");
+      ln("float a = " + Op + "::init();");
+      ln("for (int w = 0; w < wpb; ++w) a = " + Op + "::apply(a, smem[w * " + std::to_string(c.slab_floats + 32) + " + " +
+         std::to_string(c.cross_off[x]) + " + i]);");
+      ln(parts + "[" + rank + " * " + std::to_string(So) + "LL + i] = a;");
+      close();
+      ln("__syncthreads();");
     } else {
       // warps -> shared partial rows -> fixed-order CTA sum
       ln("__syncthreads();");
