@@ -66,6 +66,7 @@ int stitch_executor_create(const char* fused_graph_json, const char* options_jso
     if (o.has("lazy_inputs")) opts.codegen.lazy_inputs = o.at("lazy_inputs").as_bool();
     if (o.has("colred")) opts.codegen.colred = o.at("colred").as_bool();
     if (o.has("cross_smem")) opts.codegen.cross_smem = o.at("cross_smem").as_bool();
+    if (o.has("cross_smem_min_regs")) opts.codegen.cross_smem_min_regs = static_cast<int>(o.at("cross_smem_min_regs").as_int());
     if (o.has("colred_fused")) opts.codegen.colred_fused = o.at("colred_fused").as_bool();
     if (o.has("colred_cp_async")) opts.codegen.colred_cp_async = o.at("colred_cp_async").as_bool();
     if (o.has("colred_cols")) opts.codegen.colred_cols = static_cast<int>(o.at("colred_cols").as_int());

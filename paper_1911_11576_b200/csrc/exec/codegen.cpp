@@ -846,7 +846,7 @@ bool Builder::plan_row(Component& c) {
       regs += layout(S, 32).elems();
       extra += (S + 3) / 4 * 4;
     }
-    if (regs > 48 && (off + extra + 32) * 4 * 8 <= opts_.max_smem)
+    if (regs > opts_.cross_smem_min_regs && (off + extra + 32) * 4 * 8 <= opts_.max_smem)
       for (int x : c.cross) {
         const int in = vals_[x].operands[0];
         if (vals_[x].node->reduce_dims.size() == vals_[in].dims.size()) continue;
