@@ -1289,6 +1289,47 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
            ", " + in_ptr(v) + " + (" + r + ") * " + std::to_string(S) + "LL, " + std::to_string(S * 4) + "u, bar + " + b + ");");
       }
   };
+  // tma_early: a staged input's tile for the next row is requested as soon
+  // as this row's last reader of it is done (one CTA barrier per release
+  // point), so the next row's loads overlap this row's remaining stages.
+  const bool early_tma = opts_.tma_early && c.cta && c.tma && !c.dbuf && !c.tcp;
+  std::map<size_t, std::vector<int>> release_at;  // member index -> inputs whose last reader it is
+  if (early_tma) {
+    const size_t kEnd = c.members.size();
+    std::map<int, size_t> last;
+    for (int v : inputs_)
+      if (c.staged[v]) last[v] = 0;
+    std::function<void(int, size_t)> reads = [&](int o, size_t j) {
+      if (last.count(o)) last[o] = std::max(last[o], j);
+      if (c.cls[o] == Cls::kRowed && !c.cheap.empty() && c.cheap[o] && vals_[o].member)
+        for (int q : vals_[o].operands) reads(q, j);
+    };
+    for (size_t j = 0; j < c.members.size(); ++j) {
+      const int m = c.members[j];
+      const bool after_loop = c.cls[m] == Cls::kCross || c.cls[m] == Cls::kPost;
+      for (int o : vals_[m].operands) reads(o, after_loop ? kEnd : j);
+    }
+    for (auto& [v, j] : last) release_at[j].push_back(v);
+  }
+  auto issue_some = [&](const std::vector<int>& vs, bool with_expect) {
+    if (with_expect) ln("stitch_dev::mbar_expect_tx(bar, " + std::to_string(tma_bytes) + "u);");
+    for (int v : vs) {
+      const int64_t S = prod(vals_[v].dims, k);
+      ln("stitch_dev::bulk_g2s(slab + " + std::to_string(c.smem_off[v]) + ", " + in_ptr(v) + " + (row + gstride) * " +
+         std::to_string(S) + "LL, " + std::to_string(S * 4) + "u, bar);  // next row's " + vals_[v].id);
+    }
+  };
+  bool early_expect_done = false;
+  auto release_upto = [&](size_t idx) {
+    while (!release_at.empty() && release_at.begin()->first <= idx && release_at.begin()->first < c.members.size()) {
+      ln("__syncthreads();  // every reader of these tiles is done with this row");
+      open("if (t == 0 && row + gstride < " + rhi + ")");
+      issue_some(release_at.begin()->second, !early_expect_done);
+      close();
+      early_expect_done = true;
+      release_at.erase(release_at.begin());
+    }
+  };
   if (c.tma) {
     // TMA barriers right after the reduction scratch `red` (relative to the
     // slab, which the tcgen05 region may displace)
@@ -1297,6 +1338,12 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
               : "if (t == 0) stitch_dev::mbar_init(bar, 1);");
     ln("__syncthreads();");
     ln("unsigned phase = 0;");
+    if (early_tma) {
+      // this CTA's first row; later rows are issued from inside the loop
+      open("if (t == 0 && " + rlo + " + g0 < " + rhi + ")");
+      issue_tma(rlo + " + g0", "0");
+      close();
+    }
     if (c.dbuf) {
       ln("int buf = 0;");
       open("if (t == 0 && " + rlo + " + g0 < " + rhi + ")");
@@ -1390,9 +1437,11 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
           ln("float* sm" + std::to_string(v) + " = slab + " + std::to_string(c.smem_off[v]) + " + buf * " +
              std::to_string(c.ext_floats) + ";  // " + vals_[v].id);
     } else if (c.tma) {
-      open("if (t == 0)");
-      issue_tma("row", "0");
-      close();
+      if (!early_tma) {
+        open("if (t == 0)");
+        issue_tma("row", "0");
+        close();
+      }
       ln("stitch_dev::mbar_wait(bar, phase);");
       ln("phase ^= 1u;");
     } else {
@@ -1478,6 +1527,7 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
   auto in_comp = [&](int x) { return std::find(c.members.begin(), c.members.end(), x) != c.members.end(); };
 
   for (size_t mi = 0; mi < c.members.size(); ++mi) {
+    if (early_tma && mi > 0) release_upto(mi - 1);
     const int m = c.members[mi];
     if (c.cls[m] != Cls::kRowed) continue;
     const OpNode& op = *vals_[m].node;
@@ -1892,6 +1942,16 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
   memo_.pop_back();
   if (c.tcp) ln("tb ^= 1;");
   if (c.cta && (any_ext_staged || std::any_of(c.staged.begin(), c.staged.end(), [](char s) { return s; }))) ln("__syncthreads();");
+  if (early_tma) {
+    std::vector<int> rest;
+    for (auto& [j, vs] : release_at) rest.insert(rest.end(), vs.begin(), vs.end());
+    if (!rest.empty() || !early_expect_done) {
+      open("if (t == 0 && row + gstride < " + rhi + ")");
+      issue_some(rest, !early_expect_done);
+      close();
+    }
+    release_at.clear();
+  }
   close();  // row loop
   if (c.tc) ln("stitch_dev::tc::dealloc(tmem, " + std::string(c.tcp ? (c.tc_list.size() > 1 ? "256" : "128") : "64") + ");");
 

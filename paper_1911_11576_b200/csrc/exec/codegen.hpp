@@ -70,6 +70,7 @@ struct CodegenOptions {
   bool loop_fusion = true;
   bool colred = true;
   bool colred_fused = true;
+  bool tma_early = false;  // CTA rows: next row's TMA tiles requested as soon as their last reader is done
   bool cross_smem = true;  // warp rows: many column-reduction partials in the warp's shared slab
   int cross_smem_min_regs = 16;  // ... when they would take more than this many registers per lane
   int colred_ctas_per_sm = 4;  // COLRED tiles per SM (one resident wave)
