@@ -940,7 +940,7 @@ std::string Builder::elem_expr(const OpNode& op, const std::vector<std::string>&
     // c / x with c = +-2^k: c * rcp.rn(x) is exactly rn(c / x) (scaling by
     // a power of two commutes with rounding) at a fraction of div.rn's cost
     unsigned bits = 0;
-    if (std::sscanf(a[0].c_str(), "__int_as_float(0x%x)", &bits) == 1 && a[0].size() == 26 && (bits & 0x7fffffu) == 0 &&
+    if (opts_.rcp_divide && std::sscanf(a[0].c_str(), "__int_as_float(0x%x)", &bits) == 1 && a[0].size() == 26 && (bits & 0x7fffffu) == 0 &&
         ((bits >> 23) & 0xffu) > 0 && ((bits >> 23) & 0xffu) < 0xffu)
       return "(" + a[0] + " * __frcp_rn(" + a[1] + "))";
     return "(" + a[0] + " / " + a[1] + ")";

@@ -70,6 +70,7 @@ struct CodegenOptions {
   bool loop_fusion = true;
   bool colred = true;
   bool colred_fused = true;
+  bool rcp_divide = true;  // c / x with c = +-2^k as the exact c * rcp.rn(x)
   bool tma_early = false;  // CTA rows: next row's TMA tiles requested as soon as their last reader is done
   bool cross_smem = true;  // warp rows: many column-reduction partials in the warp's shared slab
   int cross_smem_min_regs = 16;  // ... when they would take more than this many registers per lane

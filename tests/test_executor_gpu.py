@@ -305,6 +305,37 @@ def test_colred_fused_producer(R, C, opts):
     assert np.array_equal(a[0], b[0])
 
 
+@pytest.mark.parametrize("kind", ["sum", "max"])
+@pytest.mark.parametrize("dims", [(4, 100, 132), (2, 3, 1, 8), (3, 1, 4)])
+def test_colred_fused_producer_multidim(kind, dims):
+    """COLRED over a leading multi-dimension prefix (reduce_dims [0, 1]) of a
+    producer chain with a row-invariant broadcast, sum and max."""
+    d = list(dims)
+    inner = d[2:]
+    g = {"nodes": [{"id": "a", "kind": "parameter", "shape": {"dims": d, "dtype": "f32"}},
+                   {"id": "b", "kind": "parameter", "shape": {"dims": inner, "dtype": "f32"}},
+                   {"id": "bb", "kind": "elementwise", "name": "broadcast", "operands": ["b"],
+                    "shape": {"dims": d, "dtype": "f32"}},
+                   {"id": "e", "kind": "elementwise", "name": "exp", "operands": ["a"], "shape": {"dims": d, "dtype": "f32"}},
+                   {"id": "p", "kind": "elementwise", "name": "subtract", "operands": ["e", "bb"],
+                    "shape": {"dims": d, "dtype": "f32"}},
+                   dict({"id": "r", "kind": "reduce", "operands": ["p"], "reduce_dims": [0, 1],
+                         "shape": {"dims": inner, "dtype": "f32"}}, **({"name": "max"} if kind == "max" else {}))],
+         "outputs": ["r"]}
+    fused = rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT)["fused"]
+    ins = orc.random_inputs(g, seed=sum(d))
+    ex = assert_parity(g, fused, ins)
+    if prod_(inner) % 4 == 0:
+        assert "colred" in ex.info["kernels"][0]["scheme"]
+
+
+def prod_(xs):
+    out = 1
+    for x in xs:
+        out *= x
+    return out
+
+
 @pytest.mark.parametrize("name", list(W.CONFIGS))
 def test_run_host_dataflow_copies(name):
     """stitch_executor_run_host with the dataflow copy schedule (inputs up
