@@ -62,11 +62,12 @@ struct CodegenOptions {
   int num_sms = 148;
   int max_smem = 232448 - 1024;  // per-CTA opt-in limit minus a static-smem margin
   bool allow_row = true;         // false forces SECTIONED (tests)
-  // Measured on B200 (scripts/time_graph.py): both lose to the occupancy
-  // they cost on the bench configs (layernorm 18.4 -> 24.5 us with
-  // prefetch; GRU 139 -> 170 us with a double buffer at 1 CTA/SM), so they
-  // are opt-in.
-  bool row_prefetch = false;      // prefetch the next row's register tiles
+  // Measured on B200 (scripts/time_graph.py): the double buffer loses to
+  // the occupancy it costs (GRU 139 -> 170 us at 1 CTA/SM), so it is
+  // opt-in; row prefetching (only where the prefetched tiles take <= 32
+  // registers) is neutral on the subgraph configs and takes the BERT step
+  // 2419 -> 2382 us, so it is on.
+  bool row_prefetch = true;       // prefetch the next row's register tiles
   bool loop_fusion = true;
   bool colred = true;
   bool colred_fused = true;
