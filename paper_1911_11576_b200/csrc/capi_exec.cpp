@@ -65,6 +65,7 @@ int stitch_executor_create(const char* fused_graph_json, const char* options_jso
     if (o.has("wide_cross_cta")) opts.codegen.wide_cross_cta = o.at("wide_cross_cta").as_bool();
     if (o.has("lazy_inputs")) opts.codegen.lazy_inputs = o.at("lazy_inputs").as_bool();
     if (o.has("colred")) opts.codegen.colred = o.at("colred").as_bool();
+    if (o.has("row_prefetch_warp")) opts.codegen.row_prefetch_warp = o.at("row_prefetch_warp").as_bool();
     if (o.has("rcp_divide")) opts.codegen.rcp_divide = o.at("rcp_divide").as_bool();
     if (o.has("tma_early")) opts.codegen.tma_early = o.at("tma_early").as_bool();
     if (o.has("cross_smem")) opts.codegen.cross_smem = o.at("cross_smem").as_bool();

@@ -923,7 +923,7 @@ bool Builder::plan_row(Component& c) {
   for (int v : inputs_)
     if (c.cls[v] == Cls::kRowed && !c.staged[v] && prod(vals_[v].dims, k) > 1 && reg_input(c, v))
       pf_regs += layout(prod(vals_[v].dims, k), c.NT).elems();
-  c.prefetch = opts_.row_prefetch && pf_regs > 0 && pf_regs <= 32;
+  c.prefetch = opts_.row_prefetch && pf_regs > 0 && pf_regs <= 32 && (c.cta || opts_.row_prefetch_warp);
   return true;
 }
 

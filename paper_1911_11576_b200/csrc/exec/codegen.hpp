@@ -65,9 +65,11 @@ struct CodegenOptions {
   // Measured on B200 (scripts/time_graph.py): the double buffer loses to
   // the occupancy it costs (GRU 139 -> 170 us at 1 CTA/SM), so it is
   // opt-in; row prefetching (only where the prefetched tiles take <= 32
-  // registers) is neutral on the subgraph configs and takes the BERT step
-  // 2419 -> 2382 us, so it is on.
-  bool row_prefetch = true;       // prefetch the next row's register tiles
+  // registers) helps CTA rows (BERT row_cta groups ~5 % each, step 2419 ->
+  // 2382 us) but costs warp rows occupancy (layernorm 18.4 -> 20.5 us), so
+  // it is on for CTA rows only.
+  bool row_prefetch = true;        // prefetch the next row's register tiles (CTA rows)
+  bool row_prefetch_warp = false;  // ... and warp rows
   bool loop_fusion = true;
   bool colred = true;
   bool colred_fused = true;

@@ -212,7 +212,7 @@ def test_gru_double_buffer_and_prefetch_variants():
     assert "tma2" in ex.info["kernels"][0]["scheme"]
 
 
-VARIANTS = [dict(pack_sequential=True), dict(loop_fusion=False), dict(row_prefetch=False),
+VARIANTS = [dict(pack_sequential=True), dict(loop_fusion=False), dict(row_prefetch=False), dict(row_prefetch_warp=True),
             dict(tma_double_buffer=True), dict(tensor_cores=True), dict(colred=False), dict(lazy_inputs=True),
             dict(pdl=False), dict(fold_constants=False), dict(colred_cp_async=False), dict(colred_cols=32), dict(cross_smem=False), dict(tma_early=True)]
 
