@@ -375,6 +375,22 @@ def test_bert_lazy_inputs_variant():
     assert_parity(g, fused, orc.random_inputs(g, seed=111, scale=0.5), lazy_inputs=True)
 
 
+@pytest.mark.parametrize("seed", range(0, 64, 3))
+def test_random_dag_parity_options(seed):
+    """Random DAGs through the non-default codegen paths at once: warp-row
+    prefetch, 32-column COLRED blocks, early TMA, register column partials,
+    plain COLRED loads."""
+    from helpers import random_dag
+    R = [3, 64, 100, 257, 1024, 1, 2, 4096][seed % 8]
+    C = [4, 33, 256, 768, 1000, 1, 2, 2048][(seed // 8) % 8]
+    g = random_dag(seed, n_ops=6 + seed % 10, dims=(R, C))
+    ins = orc.random_inputs(g, seed=seed, scale=0.5)
+    fused = rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT)["fused"]
+    assert_parity(g, fused, ins, row_prefetch_warp=True, colred_cols=32, tma_early=True, cross_smem=False,
+                  colred_cp_async=False)
+    assert_parity(g, g, ins, colred_cols=64, cross_smem_min_regs=0)
+
+
 @pytest.mark.parametrize("seed", range(64))
 def test_random_dag_parity(seed):
     """Seeded random graphs (elementwise chains, row and column reductions,
