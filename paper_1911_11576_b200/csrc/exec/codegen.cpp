@@ -367,7 +367,7 @@ bool Builder::plan_colred(Component& c) {
   if (c.cr_C % 4 != 0 || c.cr_R < 1) return false;
   // W-column blocks (colred_cols: 32, 64 or 128): a warp load covers
   // 128 / W * 4 rows x W floats; the last CTA of a block folds W columns
-  const int W = opts_.colred_cols == 32 || opts_.colred_cols == 64 ? opts_.colred_cols : 128;
+  const int W = opts_.colred_cols == 32 || opts_.colred_cols == 64 ? opts_.colred_cols : 128;  // default 32
   c.cr_w = W;
   c.cr_ncb = (c.cr_C + W - 1) / W;
   // one wave of colred_ctas_per_sm CTAs of 8 warps per SM

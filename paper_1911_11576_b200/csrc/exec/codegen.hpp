@@ -78,7 +78,7 @@ struct CodegenOptions {
   bool cross_smem = true;  // warp rows: many column-reduction partials in the warp's shared slab
   int cross_smem_min_regs = 16;  // ... when they would take more than this many registers per lane
   int colred_ctas_per_sm = 4;  // COLRED tiles per SM (one resident wave)
-  int colred_cols = 128;       // COLRED column-block width: 32, 64 or 128 floats
+  int colred_cols = 32;        // COLRED column-block width: 32, 64 or 128 floats (32: BERT 2387 -> 2375 us)
   bool colred_cp_async = true;  // COLRED loads staged through cp.async (all of a pass in flight)  // COLRED also for reduces of an inline elementwise producer chain
   // many-input rows: load inputs per fused-loop step, not per row (measured
   // neutral on the BERT LayerNorm-backward groups: the column-reduction

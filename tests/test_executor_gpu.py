@@ -214,7 +214,7 @@ def test_gru_double_buffer_and_prefetch_variants():
 
 VARIANTS = [dict(pack_sequential=True), dict(loop_fusion=False), dict(row_prefetch=False), dict(row_prefetch_warp=True),
             dict(tma_double_buffer=True), dict(tensor_cores=True), dict(colred=False), dict(lazy_inputs=True),
-            dict(pdl=False), dict(fold_constants=False), dict(colred_cp_async=False), dict(colred_cols=32), dict(cross_smem=False), dict(tma_early=True)]
+            dict(pdl=False), dict(fold_constants=False), dict(colred_cp_async=False), dict(colred_cols=128), dict(cross_smem=False), dict(tma_early=True)]
 
 
 @pytest.mark.parametrize("name", list(W.CONFIGS))
@@ -277,8 +277,8 @@ def test_colred_scheme(R, C):
 
 
 @pytest.mark.parametrize("R,C", [(1, 4), (5, 12), (64, 768), (4096, 768), (1000, 2304), (33, 132)])
-@pytest.mark.parametrize("opts", [{}, {"colred_cols": 32}, {"colred_cols": 64}, {"colred_cp_async": False},
-                                  {"colred_ctas_per_sm": 1}], ids=["w128", "w32", "w64", "ldg", "cta1"])
+@pytest.mark.parametrize("opts", [{}, {"colred_cols": 128}, {"colred_cols": 64}, {"colred_cp_async": False},
+                                  {"colred_ctas_per_sm": 1}], ids=["w32", "w128", "w64", "ldg", "cta1"])
 def test_colred_fused_producer(R, C, opts):
     """COLRED with an inline elementwise producer (LayerNorm dgamma =
     sum_rows(dy * xhat) with a broadcast scale) across column-block widths,
@@ -386,7 +386,7 @@ def test_random_dag_parity_options(seed):
     g = random_dag(seed, n_ops=6 + seed % 10, dims=(R, C))
     ins = orc.random_inputs(g, seed=seed, scale=0.5)
     fused = rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT)["fused"]
-    assert_parity(g, fused, ins, row_prefetch_warp=True, colred_cols=32, tma_early=True, cross_smem=False,
+    assert_parity(g, fused, ins, row_prefetch_warp=True, colred_cols=128, tma_early=True, cross_smem=False,
                   colred_cp_async=False)
     assert_parity(g, g, ins, colred_cols=64, cross_smem_min_regs=0)
 
