@@ -9,32 +9,37 @@ graph (SPEC fusion-transform Non-goals), so its op semantics are defined by
 the C expressions its emitter writes for each op. This interpreter restates
 them op by op, in float64 by default:
 
-  add/subtract/multiply/divide   a+b, a-b, a*b, a/b     emitter.cpp:810-813
-  maximum/minimum                fmaxf / fminf          emitter.cpp:814-815
-  log/exp/negate/rsqrt           logf/expf/-(x)/rsqrtf  emitter.cpp:816-819
-  compare                        (a > b) ? 1 : 0        emitter.cpp:820-824
-  select                         (p != 0) ? a : b       emitter.cpp:825-828
+  add/subtract/multiply/divide   a+b, a-b, a*b, a/b     emitter.cpp:897-900
+  maximum/minimum                fmaxf / fminf          emitter.cpp:901-902
+  log/exp/negate/rsqrt           logf/expf/-(x)/rsqrtf  emitter.cpp:903-906
+  compare                        (a > b) ? 1 : 0        emitter.cpp:907-911
+  select                         (p != 0) ? a : b       emitter.cpp:912-915
   broadcast                      in[coords[map[i]]], map = right-most greedy
-                                 subsequence match      graph.cpp:146, emitter.cpp:801
-  reduce                         sum over reduce_dims   emitter.cpp:720-744
-                                 (extension: "name": "max" -> max)
+                                 subsequence match      graph.cpp:158, emitter.cpp:890-895
+  reduce                         sum over reduce_dims   emitter.cpp:808-831
+                                 (extension: "name": "max" -> max; the
+                                 reference emitter sums every reduce)
   dot                            sum_k lhs[..k..]*rhs[..k..], output dims =
                                  lhs minus cd0 then rhs minus cd1
-                                                        emitter.cpp:746-786
-  batched_dot                    per batch [M,K] x [K,N] emitter.cpp:765-776
+                                                        emitter.cpp:833-876
+  batched_dot                    per batch [M,K] x [K,N] emitter.cpp:850-861
   constant                       the node's "value" (extension; the reference
-                                 has no constant data)
+                                 has no constant data -- its kernels take
+                                 constants as pointer arguments)
 
-The restatement is pinned against the reference's own emitted kernels run on
-a B200 (tests/test_ref_sketches.py) and against the reference planner through
-oracle/_ref for everything structural.
+Pinned: the reference's own emitted kernels (tests/golden/ref_sketches.json,
+from oracle/_ref for the six reference fixtures and the SMALL configs, fused
+and one-kernel-per-op) are compiled for sm_100a and run on a B200 by
+oracle/ref_sketches.py; tests/test_ref_sketches.py checks this interpreter
+against their outputs at the stated tolerance. Everything structural (plans,
+indexing) is checked against the reference planner through oracle/_ref.
 """
 
 import numpy as np
 
 
 def broadcast_dim_map(in_dims, out_dims):
-    """Right-most greedy subsequence match (reference graph.cpp:146)."""
+    """Right-most greedy subsequence match (reference graph.cpp:158)."""
     m = [-1] * len(in_dims)
     o = len(out_dims) - 1
     for i in range(len(in_dims) - 1, -1, -1):

@@ -1,7 +1,7 @@
 // Stitched-kernel generator (see codegen.hpp for the scheme overview).
 //
 // Value semantics follow the reference emitter's per-op C expressions
-// (proj/src/emitter.cpp:793-829) and broadcast indexing (graph.cpp:146):
+// (proj/src/emitter.cpp:883-915) and broadcast indexing (graph.cpp:158):
 // out[c] = in[c[map[0]], ..., c[map[r-1]]] with map the right-most greedy
 // subsequence match. Reductions: sum (reference) or max (extension).
 #include "codegen.hpp"

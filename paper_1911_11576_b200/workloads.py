@@ -146,7 +146,7 @@ def softmax(heads=64, seq=512):
     scores, stored as rows [heads*seq, seq] with an additive key mask [seq].
 
     Why 2-D: the IR's broadcast has no explicit dimension list; it maps input
-    dims onto output dims right-most-greedily (reference graph.cpp:146
+    dims onto output dims right-most-greedily (reference graph.cpp:158
     broadcast_dim_map). A row statistic [heads, seq] broadcast back to
     [heads, seq, seq] would land on dims (0, 2) -- a column broadcast -- because
     both trailing extents are 512. Flattening (head, query) into one row axis
