@@ -1,6 +1,10 @@
 """Benchmark: fused-subgraph GB/s of the stitched executor on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl stitch|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl stitch|reference] [--dry-run]
+
+--gpus N without a torchrun environment re-launches this script under
+`torch.distributed.run --nproc-per-node N` (one process per GPU, 127.0.0.1
+rendezvous); under torchrun WORLD_SIZE must equal N.
 
 One step = one pass of every BASELINE.json subgraph config (the suite in
 paper_1911_11576_b200/workloads.py, per-GPU batch shard each) through its
@@ -54,6 +58,8 @@ def parse_args():
     ap.add_argument("--no-unfused", action="store_true")
     ap.add_argument("--no-model-plan", action="store_true")
     ap.add_argument("--out", default="", help="also write the JSON line to this file")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU check of the rank plumbing: gloo, compile-only executors, host-timed stub steps")
     return ap.parse_args()
 
 
@@ -62,6 +68,30 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
+
+
+def _free_port():
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch_if_needed(args):
+    """--gpus N with no torchrun environment: re-exec under
+    torch.distributed.run with N local ranks and return its exit code;
+    None when this process is already the right rank."""
+    if "WORLD_SIZE" in os.environ:
+        world = int(os.environ["WORLD_SIZE"])
+        if world != args.gpus:
+            raise SystemExit("bench.py: --gpus %d but WORLD_SIZE=%d" % (args.gpus, world))
+        return None
+    if args.gpus <= 1:
+        return None
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def suite_names(args):
@@ -286,11 +316,70 @@ def emit(line, args):
 # GPU leg
 # ---------------------------------------------------------------------------
 
+def plan_digest(fused):
+    import hashlib
+    return hashlib.sha1(json.dumps(fused, sort_keys=True).encode()).hexdigest()[:16]
+
+
+def run_dry(args, world, rank):
+    """--dry-run: the multi-rank bench plumbing on CPU (gloo) -- per-rank
+    plans and compile-only executors, identical plans across ranks
+    (all-gathered digests), barrier-bracketed host-timed stub steps and the
+    max-over-ranks step time; rank 0 prints the JSON line."""
+    import torch
+    import torch.distributed as dist
+    from paper_1911_11576_b200 import runtime as rt
+    from paper_1911_11576_b200 import tuning
+    from paper_1911_11576_b200 import workloads as W
+
+    if world > 1:
+        dist.init_process_group("gloo")
+    names = suite_names(args)
+    digests, total_bytes, kernels = [], 0, 0
+    for name in names:
+        g = W.CONFIGS[name]()
+        plan, _ = tuning.config_plan(name, g)
+        ex = rt.Executor(plan["fused"], compile_only=True)
+        digests.append(plan_digest(plan["fused"]))
+        total_bytes += graph_bytes(g)
+        kernels += len(ex.info["kernels"])
+    if world > 1:
+        every = [None] * world
+        dist.all_gather_object(every, digests)
+        assert all(d == digests for d in every), "ranks planned different fusion groups"
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        time.sleep(0.001 * (1 + rank))  # stub step: rank-dependent so the max is visible
+    if world > 1:
+        dist.barrier()
+    ms = torch.tensor([(time.perf_counter() - t0) * 1e3 / max(1, args.steps)], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    line = {"metric": "fused-subgraph GB/s", "value": None, "stub_GBps": world * total_bytes / (float(ms.item()) * 1e-3) / 1e9,
+            "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": float(ms.item()), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "dry run: no kernels launched, host-timed stub steps",
+            "dry_run": True, "plan_digests": dict(zip(names, digests)),
+            "config": {"workload": "suite:" + ",".join(names), "parallelism": "batch-sharded dp%d, no collectives" % world},
+            "gpu_launches": 0, "kernels_per_step": kernels}
+    if rank == 0:
+        emit(line, args)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse_args()
+    rc = relaunch_if_needed(args)
+    if rc is not None:
+        sys.exit(rc)
     world, rank, local = dist_env()
     if args.impl == "reference":
         run_reference(args, world, rank)
+        return
+    if args.dry_run:
+        run_dry(args, world, rank)
         return
 
     import torch

@@ -2253,10 +2253,16 @@ KernelSpec Builder::build() {
         const int64_t So = scalar ? 1 : prod(vals_[in].dims, c.k);
         ws_off_[x] = ws_floats_;
         ws_floats_ += max_ctas * ((So + 63) / 64 * 64);
-        if (!c.post.empty() && !vals_[x].output) {
-          int64_t off = ws_floats_;
-          ws_floats_ += (So + 63) / 64 * 64;
-          materialized_[x] = "(ws + " + std::to_string(off) + "LL)";
+        if (!c.post.empty()) {
+          // post-reduction ops read the finished reduce after the second
+          // grid barrier: from its output buffer, or a workspace row
+          if (vals_[x].output) {
+            materialized_[x] = out_ptr(x);
+          } else {
+            int64_t off = ws_floats_;
+            ws_floats_ += (So + 63) / 64 * 64;
+            materialized_[x] = "(ws + " + std::to_string(off) + "LL)";
+          }
         }
       }
     for (Component& c : comps)

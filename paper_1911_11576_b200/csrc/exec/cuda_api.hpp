@@ -19,6 +19,9 @@ struct CudaApi {
   STITCH_CU_FN(cuCtxGetCurrent)
   STITCH_CU_FN(cuCtxSetCurrent)
   STITCH_CU_FN(cuDevicePrimaryCtxRetain)
+  STITCH_CU_FN(cuDevicePrimaryCtxRelease)
+  STITCH_CU_FN(cuCtxPushCurrent)
+  STITCH_CU_FN(cuCtxPopCurrent)
   STITCH_CU_FN(cuModuleLoadData)
   STITCH_CU_FN(cuModuleUnload)
   STITCH_CU_FN(cuModuleGetFunction)
@@ -72,6 +75,9 @@ struct CudaApi {
     STITCH_CU_LOAD(cuCtxGetCurrent, "cuCtxGetCurrent")
     STITCH_CU_LOAD(cuCtxSetCurrent, "cuCtxSetCurrent")
     STITCH_CU_LOAD(cuDevicePrimaryCtxRetain, "cuDevicePrimaryCtxRetain")
+    STITCH_CU_LOAD(cuDevicePrimaryCtxRelease, "cuDevicePrimaryCtxRelease_v2")
+    STITCH_CU_LOAD(cuCtxPushCurrent, "cuCtxPushCurrent_v2")
+    STITCH_CU_LOAD(cuCtxPopCurrent, "cuCtxPopCurrent_v2")
     STITCH_CU_LOAD(cuModuleLoadData, "cuModuleLoadData")
     STITCH_CU_LOAD(cuModuleUnload, "cuModuleUnload")
     STITCH_CU_LOAD(cuModuleGetFunction, "cuModuleGetFunction")
@@ -112,6 +118,26 @@ inline void cu_check(CUresult r, const char* what) {
   CudaApi::get().cuGetErrorString(r, &msg);
   throw std::runtime_error(std::string("CUDA error in ") + what + ": " + (msg ? msg : "unknown"));
 }
+
+// Makes `ctx` current on the calling thread for a scope (the executor's
+// device primary context, whatever context the caller has current).
+class CtxScope {
+ public:
+  explicit CtxScope(void* ctx) : on_(ctx != nullptr) {
+    if (on_) cu_check(CudaApi::get().cuCtxPushCurrent(static_cast<CUcontext>(ctx)), "cuCtxPushCurrent");
+  }
+  ~CtxScope() {
+    if (on_) {
+      CUcontext old;
+      CudaApi::get().cuCtxPopCurrent(&old);
+    }
+  }
+  CtxScope(const CtxScope&) = delete;
+  CtxScope& operator=(const CtxScope&) = delete;
+
+ private:
+  bool on_;
+};
 
 }  // namespace exec
 }  // namespace stitch

@@ -124,8 +124,10 @@ Executor::Executor(const Graph& fused, const ExecOptions& opts) : g_(fused), opt
 }
 
 Executor::~Executor() {
-  if (!device_ready_) return;
+  if (!ctx_) return;
   CudaApi& cu = CudaApi::get();
+  {
+  CtxScope scope(ctx_);
   if (graph_exec_) cu.cuGraphExecDestroy(static_cast<CUgraphExec>(graph_exec_));
   for (void* e : in_events_) cu.cuEventDestroy(static_cast<CUevent>(e));
   for (void* e : kernel_events_) cu.cuEventDestroy(static_cast<CUevent>(e));
@@ -141,6 +143,9 @@ Executor::~Executor() {
   if (sync_) cu.cuMemFree(sync_);
   for (uint64_t p : host_staging_)
     if (p) cu.cuMemFree(p);
+  }
+  CUdevice dev;
+  if (cu.cuDeviceGet(&dev, opts_.device) == CUDA_SUCCESS) cu.cuDevicePrimaryCtxRelease(dev);
 }
 
 void Executor::build_kernels() {
@@ -326,11 +331,24 @@ void Executor::plan_chunks() {
         if (inter / C <= opts_.chunk_l2_bytes) break;
       }
       seg.chunks = best;
-      if (best > 1)
+      if (best > 1) {
         for (int b : local) {
           bufs_[b].chunks = best;
           bufs_[b].ring = opts_.chunk_pipeline ? std::min(best, std::max(1, opts_.chunk_ring)) : 1;
         }
+        // A chunked segment runs all of its kernels once per chunk, so any
+        // buffer it touches is live across the whole segment (not just its
+        // own kernel-index interval): widen lifetimes before plan_arena so
+        // no chunk ring is placed on top of a value a later chunk still
+        // writes or reads.
+        for (int k = seg.first; k <= seg.last; ++k) {
+          for (const std::vector<int>* v : {&kernels_[k].in_bufs, &kernels_[k].out_bufs})
+            for (int b : *v) {
+              bufs_[b].first = std::min(bufs_[b].first, seg.first);
+              bufs_[b].last = std::max(bufs_[b].last, seg.last);
+            }
+        }
+      }
     }
     segments_.push_back(seg);
   }
@@ -373,14 +391,15 @@ void Executor::plan_arena() {
 void Executor::init_device() {
   CudaApi& cu = CudaApi::get();
   cu_check(cu.cuInit(0), "cuInit");
-  CUcontext ctx = nullptr;
-  cu_check(cu.cuCtxGetCurrent(&ctx), "cuCtxGetCurrent");
   CUdevice dev;
   cu_check(cu.cuDeviceGet(&dev, opts_.device), "cuDeviceGet");
-  if (!ctx) {
-    cu_check(cu.cuDevicePrimaryCtxRetain(&ctx, dev), "cuDevicePrimaryCtxRetain");
-    cu_check(cu.cuCtxSetCurrent(ctx), "cuCtxSetCurrent");
-  }
+  // Always the primary context of opts_.device (the one torch / the CUDA
+  // runtime use for that device), made current around every call, whatever
+  // context the calling thread has current.
+  CUcontext ctx = nullptr;
+  cu_check(cu.cuDevicePrimaryCtxRetain(&ctx, dev), "cuDevicePrimaryCtxRetain");
+  ctx_ = ctx;
+  CtxScope scope(ctx_);
   cu_check(cu.cuDeviceGetAttribute(&sms_, CU_DEVICE_ATTRIBUTE_MULTIPROCESSOR_COUNT, dev), "sm count");
   int major = 0, minor = 0;
   cu.cuDeviceGetAttribute(&major, CU_DEVICE_ATTRIBUTE_COMPUTE_CAPABILITY_MAJOR, dev);
@@ -474,15 +493,15 @@ void Executor::launch_one(int i, int c, int chunks, const void* const* inputs, v
     return arena_ + x.offset + static_cast<CUdeviceptr>(c % x.ring) * cb - static_cast<CUdeviceptr>(c) * cb;
   };
   KernelInst& k = kernels_[i];
-  CUdeviceptr vals[64];
+  const size_t nargs = k.in_bufs.size() + k.out_bufs.size() + 2;
+  std::vector<CUdeviceptr> vals(nargs);
   long long rng[2];
-  void* args[66];
+  std::vector<void*> args(nargs + 2);
   int na = 0;
   for (int b : k.in_bufs) vals[na++] = addr(b);
   for (int b : k.out_bufs) vals[na++] = addr(b);
   vals[na++] = ws_ + k.ws_off * 4;
   vals[na++] = sync_ + k.sync_off * 4;
-  if (na > 64) throw std::runtime_error("kernel " + k.spec.name + " has too many arguments");
   for (int a = 0; a < na; ++a) args[a] = &vals[a];
   int grid = k.grid;
   rng[0] = rng[1] = 0;
@@ -520,7 +539,7 @@ void Executor::launch_one(int i, int c, int chunks, const void* const* inputs, v
     cfg.attrs = attr;
     cfg.numAttrs = 1;
   }
-  cu_check(cu.cuLaunchKernelEx(&cfg, static_cast<CUfunction>(k.fn), args, nullptr), k.spec.name.c_str());
+  cu_check(cu.cuLaunchKernelEx(&cfg, static_cast<CUfunction>(k.fn), args.data(), nullptr), k.spec.name.c_str());
 }
 
 void Executor::launch_all(const void* const* inputs, void* const* outputs, void* stream, std::vector<void*>* events) {
@@ -576,6 +595,7 @@ void Executor::launch_all(const void* const* inputs, void* const* outputs, void*
 void Executor::run(const void* const* inputs, void* const* outputs, void* stream) {
   if (!device_ready_) throw std::runtime_error("executor was created compile-only");
   CudaApi& cu = CudaApi::get();
+  CtxScope scope(ctx_);
   if (!opts_.use_graph || stream == nullptr) {
     launch_all(inputs, outputs, stream, nullptr);
     return;
@@ -607,7 +627,9 @@ void Executor::run(const void* const* inputs, void* const* outputs, void* stream
 }
 
 void Executor::run_host(const void* const* host_inputs, void* const* host_outputs, void* stream) {
+  if (!device_ready_) throw std::runtime_error("executor was created compile-only");
   CudaApi& cu = CudaApi::get();
+  CtxScope scope(ctx_);
   const size_t ni = input_ids_.size(), no = output_ids_.size();
   if (host_staging_.empty()) {
     host_staging_.resize(ni + no, 0);
@@ -730,7 +752,9 @@ bool Executor::segments_ok_for_overlap() const {
 }
 
 json::Value Executor::profile(const void* const* inputs, void* const* outputs, void* stream, int iters) {
+  if (!device_ready_) throw std::runtime_error("executor was created compile-only");
   CudaApi& cu = CudaApi::get();
+  CtxScope scope(ctx_);
   std::vector<void*> ev(2 * launches_per_run_);
   for (void*& e : ev) {
     CUevent x;

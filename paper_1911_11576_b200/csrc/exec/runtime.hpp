@@ -134,6 +134,7 @@ class Executor {
   uint64_t arena_ = 0, ws_ = 0, sync_ = 0;  // CUdeviceptr
   int sms_ = 148;
   bool device_ready_ = false;
+  void* ctx_ = nullptr;  // retained primary context of opts_.device
   // CUDA-graph replay cache for the last pointer set
   void* graph_exec_ = nullptr;
   void* graph_stream_ = nullptr;

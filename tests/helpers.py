@@ -46,3 +46,25 @@ def random_dag(seed, n_ops=12, dims=(64, 256), reduce_p=0.2):
 def scaled_inputs(graph, seed=0, scale=0.5):
     from oracle import executor as orc
     return orc.random_inputs(graph, seed=seed, scale=scale)
+
+
+def _node(i, k, ops=None, name=None, dims=(4096, 256), **kw):
+    d = {"id": i, "kind": k, "shape": {"dims": list(dims), "dtype": "f32"}}
+    if ops:
+        d["operands"] = ops
+    if name:
+        d["name"] = name
+    d.update(kw)
+    return d
+
+
+def chunk_chain_graph(R=4096, C=256):
+    """exp -> multiply -> add (three chunkable kernels, unfused) feeding a
+    column reduce that cannot be chunked."""
+    return {"nodes": [_node("x", "parameter", dims=(R, C)),
+                      _node("a", "elementwise", ["x"], "exp", dims=(R, C)),
+                      _node("b", "elementwise", ["a", "x"], "multiply", dims=(R, C)),
+                      _node("y", "elementwise", ["b", "x"], "add", dims=(R, C)),
+                      _node("cs", "reduce", ["y"], dims=(C,), reduce_dims=[0])],
+            "outputs": ["cs"]}
+

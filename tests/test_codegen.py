@@ -7,6 +7,8 @@ from paper_1911_11576_b200 import runtime as rt
 from paper_1911_11576_b200 import tuning
 from paper_1911_11576_b200 import workloads as W
 
+from helpers import _node, chunk_chain_graph
+
 
 def compile_only(fused, **kw):
     return rt.Executor(fused, compile_only=True, **kw)
@@ -54,3 +56,29 @@ def test_unfused_baseline_one_kernel_per_op():
     ex = compile_only(g, fold_constants=False)  # the bench's unfused baseline
     ops = [n for n in g["nodes"] if n["kind"] in ("elementwise", "reduce", "dot", "batched_dot")]
     assert len(ex.info["kernels"]) == len(ops)
+
+
+def test_chunked_segment_buffers_do_not_alias():
+    """every buffer a chunked segment touches is live across the
+    whole segment (each chunk runs all of its kernels), so `y` -- written by
+    the segment's last kernel, read after it -- may not share memory with
+    the chunk rings of `a` and `b`: 4 MiB + 2 rings of 2 x 2 MiB."""
+    ex = compile_only(chunk_chain_graph(), chunking=True, chunk_fill=False)
+    assert ex.info["schedule"][0]["chunks"] == 2 and len(ex.info["schedule"][0]["kernels"]) == 3
+    assert ex.info["arena_bytes"] >= 12 * 2 ** 20
+
+
+def test_colred_output_feeding_post_op_compiles():
+    """a cross-row reduce that is a graph output AND feeds a
+    post-reduction op of the same group is read back from its output."""
+    R, C = 256, 64
+    g = {"nodes": [_node("dy", "parameter", dims=(R, C)), _node("x", "parameter", dims=(R, C)),
+                   _node("p", "elementwise", ["dy", "x"], "multiply", dims=(R, C)),
+                   _node("rs", "reduce", ["p"], dims=(R,), reduce_dims=[1]),
+                   _node("db", "reduce", ["dy"], dims=(C,), reduce_dims=[0]),
+                   _node("q", "elementwise", ["db", "db"], "multiply", dims=(C,)),
+                   {"id": "t", "kind": "tuple", "operands": ["rs", "db", "q"], "shape": {"dims": [C], "dtype": "f32"}}],
+         "outputs": ["t"]}
+    fused = rt.plan(g)["fused"]
+    assert sum(n["kind"] == "fused" for n in fused["nodes"]) == 1
+    compile_only(fused)

@@ -407,3 +407,58 @@ def test_random_dag_parity(seed):
         assert_parity(g, rt.plan(g, shared_limit_bytes=lim)["fused"], ins)
     assert_parity(g, g, ins)
     assert_parity(g, rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT)["fused"], ins, allow_row=False)
+
+
+def test_chunked_segment_feeding_unchunked_consumer():
+    """a 3-kernel chunked segment whose last output feeds a
+    non-chunkable column reduce -- bit-identical to the unchunked schedule
+    and within tolerance of the oracle."""
+    from helpers import chunk_chain_graph
+    g = chunk_chain_graph()
+    ins = orc.random_inputs(g, seed=61, scale=0.5)
+    ex_c, a = run_device(g, ins, chunking=True, chunk_fill=False)
+    assert ex_c.info["schedule"][0]["chunks"] > 1
+    _, b = run_device(g, ins, chunking=False)
+    assert np.array_equal(a[0], b[0])
+    ref, bound = tolerance.reference_with_bound(g, ins)
+    ok, worst = tolerance.check(a[0], ref[0], bound[0])
+    assert ok, worst
+
+
+def test_colred_output_feeding_post_op():
+    from helpers import _node
+    R, C = 300, 64
+    g = {"nodes": [_node("dy", "parameter", dims=(R, C)), _node("x", "parameter", dims=(R, C)),
+                   _node("p", "elementwise", ["dy", "x"], "multiply", dims=(R, C)),
+                   _node("rs", "reduce", ["p"], dims=(R,), reduce_dims=[1]),
+                   _node("db", "reduce", ["dy"], dims=(C,), reduce_dims=[0]),
+                   _node("q", "elementwise", ["db", "db"], "multiply", dims=(C,)),
+                   {"id": "t", "kind": "tuple", "operands": ["rs", "db", "q"], "shape": {"dims": [C], "dtype": "f32"}}],
+         "outputs": ["t"]}
+    assert_parity(g, rt.plan(g)["fused"], orc.random_inputs(g, seed=62))
+
+
+def test_executor_uses_its_own_device_context():
+    """the executor makes its device's primary context current
+    around every call -- runs from a thread with no current context."""
+    import threading
+    g = W.layernorm(rows=64, cols=256)
+    ins = orc.random_inputs(g, seed=63)
+    ex = rt.Executor(rt.plan(g)["fused"], device=0, use_graph=False)
+    host_in = [np.ascontiguousarray(ins[i]) for i in ex.input_ids]
+    host_out = [np.empty(t["dims"], np.float32) for t in ex.info["outputs"]]
+    err = []
+
+    def work():
+        try:
+            ex.run_host(host_in, host_out)
+        except Exception as e:  # noqa: BLE001
+            err.append(e)
+
+    t = threading.Thread(target=work)
+    t.start()
+    t.join()
+    assert not err, err
+    ref, bound = tolerance.reference_with_bound(g, ins)
+    for o, r, b in zip(host_out, ref, bound):
+        assert tolerance.check(o, r, b)[0]

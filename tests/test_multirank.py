@@ -95,3 +95,32 @@ def test_shard_range_balanced():
             assert rs[0][0] == 0 and rs[-1][1] == b
             assert all(rs[i][1] == rs[i + 1][0] for i in range(w - 1))
             assert max(h - l for l, h in rs) - min(h - l for l, h in rs) <= 1
+
+
+def _bench(*args, env=None):
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    e = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    e.update(env or {})
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py")] + list(args), capture_output=True,
+                       text=True, timeout=600, env=e, cwd=root)
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    return r.returncode, (json.loads(lines[-1]) if lines else None), r.stderr
+
+
+def test_bench_gpus_2_spawns_ranks():
+    """`bench.py --gpus 2` with no torchrun environment re-launches itself
+    with two ranks; rank 0 prints one line with n_gpus 2, identical plans on
+    both ranks and the max-over-ranks step time (rank 1 sleeps 2 ms/step)."""
+    rc, line, err = _bench("--gpus", "2", "--dry-run", "--configs", "layernorm,gru", "--steps", "4", "--warmup", "1")
+    assert rc == 0, err[-2000:]
+    assert line["n_gpus"] == 2 and line["dry_run"] and line["value"] is None
+    assert set(line["plan_digests"]) == {"layernorm", "gru"}
+    assert line["ms_per_step"] >= 2.0
+
+
+def test_bench_rejects_world_size_mismatch():
+    rc, line, err = _bench("--gpus", "4", "--dry-run", env={"WORLD_SIZE": "2", "RANK": "0", "LOCAL_RANK": "0"})
+    assert rc != 0 and line is None and "WORLD_SIZE=2" in err
