@@ -380,7 +380,7 @@ SMALL = {
     "softmax": dict(heads=2, seq=128),
     "encoder": dict(batch=2, seq=64, hidden=1024),
     "gru": dict(batch=64, n=64),
-    "bert": dict(layers=1, batch=2, seq=32, hidden=64, heads=2, inter=256),
+    "bert": dict(layers=1, batch=2, seq=48, hidden=64, heads=2, inter=256),
 }
 
 # Per-GPU batch extent of each config (the shard axis) and the keyword that

@@ -110,6 +110,13 @@ def cases():
         yield "fixture:" + os.path.basename(p)[:-5], json.load(open(p))
     for name, fn in W.CONFIGS.items():
         yield name + "/small", fn(**W.SMALL[name])
+    # A square LayerNorm: its row statistics [64] broadcast to [64, 64] map
+    # onto the LAST dim under the IR's right-most-greedy rule (graph.cpp:158),
+    # i.e. the graph means a column broadcast. The reference's fused kernel
+    # reads the statistic for the CTA's own row instead (its block-scope value
+    # cache ignores the broadcast map) -- a reference emitter inconsistency the
+    # GPU test demonstrates; its unfused kernels follow the IR.
+    yield "ambiguous:layernorm64x64", W.layernorm(rows=64, cols=64)
 
 
 def main():

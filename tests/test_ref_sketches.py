@@ -35,6 +35,14 @@ VARIANTS = [(e["name"], v) for e in GOLDEN for v in e["variants"]]
 # softmax rows are shifted by the row SUM in the reference op set (its
 # emitter has no max reduce): keep exp() in range
 SCALE = {"softmax/small": 0.25, "bert/small": 0.25}
+# Graphs whose broadcasts are ambiguous under the IR's right-most-greedy
+# rule (graph.cpp:158): the reference's FUSED kernels read a row statistic
+# for the CTA's own row where the IR (and the reference's own unfused
+# kernels) index it by column -- a reference emitter inconsistency
+# (emitter.cpp value_of serves block-scope values without applying
+# broadcast_dim_map). Its unfused kernels pin the oracle there; ours follow
+# the IR.
+REF_FUSED_DEVIATES = {"ambiguous:layernorm64x64"}
 
 
 def _inputs(name, seed=5):
@@ -57,6 +65,26 @@ def test_golden_well_formed():
         # every graph output is written by some reference kernel
         written = {a for ks in e["variants"].values() for k in ks for a, o in S.signature(k["source"])[1] if o}
         assert {S.sanitize(o) for o in orc.graph_outputs(e["graph"])} <= written
+
+
+def test_bench_configs_have_unambiguous_broadcasts():
+    """Every broadcast of every bench config (SMALL and full) has exactly one
+    embedding of its input dims into its output dims, so the IR's
+    right-most-greedy map is the intended one (and the reference's fused
+    kernels agree with its unfused ones)."""
+    import itertools
+    from paper_1911_11576_b200 import workloads as W
+    for name, fn in W.CONFIGS.items():
+        for kw in (W.SMALL[name], {}):
+            g = fn(**kw)
+            nodes = {n["id"]: n for n in g["nodes"]}
+            for n in g["nodes"]:
+                if n.get("name") != "broadcast":
+                    continue
+                i, o = nodes[n["operands"][0]]["shape"]["dims"], n["shape"]["dims"]
+                embs = [c for c in itertools.combinations(range(len(o)), len(i))
+                        if all(o[c[k]] == i[k] for k in range(len(i)))]
+                assert len(embs) == 1 or not i, (name, kw, n["id"], i, o)
 
 
 def test_fig1_reference_sketch_shared_plan():
@@ -109,9 +137,14 @@ def test_ref_sketch_pins_oracle(name, variant):
     e = BY_NAME[name]
     got = _ref_run(name, variant)
     ref, bound = tolerance.reference_with_bound(e["graph"], _inputs(name))
+    worst_all = 0.0
     for oid, r, b in zip(orc.graph_outputs(e["graph"]), ref, bound):
         ok, worst = tolerance.check(got[oid], r, b)
-        assert ok, "%s %s output %s: worst err/tol %.3g" % (name, variant, oid, worst)
+        worst_all = max(worst_all, worst)
+        if name not in REF_FUSED_DEVIATES or variant == "unfused":
+            assert ok, "%s %s output %s: worst err/tol %.3g" % (name, variant, oid, worst)
+    if name in REF_FUSED_DEVIATES and variant != "unfused":
+        assert worst_all > 1.0, "the reference's fused kernel was expected to deviate from the IR here"
 
 
 @pytest.mark.gpu
@@ -119,6 +152,8 @@ def test_ref_sketch_pins_oracle(name, variant):
 def test_ref_sketch_fused_equals_unfused(name):
     """The reference's fused kernels and its one-kernel-per-op kernels agree
     (both within tolerance of each other's fp64 value)."""
+    if name in REF_FUSED_DEVIATES:
+        pytest.skip("reference fused kernels deviate from the IR on ambiguous broadcasts (see REF_FUSED_DEVIATES)")
     e = BY_NAME[name]
     ref, bound = tolerance.reference_with_bound(e["graph"], _inputs(name))
     un = _ref_run(name, "unfused")
@@ -154,7 +189,7 @@ def test_fixture_gpu_parity(name, lim):
     d_out = [torch.full(t["dims"], float("nan"), dtype=torch.float32, device="cuda") for t in ex.info["outputs"]]
     ex.run(d_in, d_out, stream=torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
-    refk = _ref_run(name, "unfused" if lim == "unfused" else
+    refk = _ref_run(name, "unfused" if lim == "unfused" or name in REF_FUSED_DEVIATES else
                     "fused@%d" % (W.B200_SHARED_LIMIT if lim == "b200" else W.REFERENCE_SHARED_LIMIT))
     ref, bound = tolerance.reference_with_bound(g, ins)
     for oid, o, r, b in zip(ex.output_ids, d_out, ref, bound):
