@@ -192,7 +192,8 @@ def test_fixture_gpu_parity(name, lim):
     refk = _ref_run(name, "unfused" if lim == "unfused" or name in REF_FUSED_DEVIATES else
                     "fused@%d" % (W.B200_SHARED_LIMIT if lim == "b200" else W.REFERENCE_SHARED_LIMIT))
     ref, bound = tolerance.reference_with_bound(g, ins)
-    for oid, o, r, b in zip(ex.output_ids, d_out, ref, bound):
+    # executor outputs follow the source graph's output order
+    for oid, o, r, b in zip(orc.graph_outputs(g), d_out, ref, bound):
         got = o.cpu().numpy()
         ok, worst = tolerance.check(got, r, b)
         assert ok, "%s output %s vs oracle: worst err/tol %.3g" % (name, oid, worst)
