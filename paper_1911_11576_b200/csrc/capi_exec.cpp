@@ -67,6 +67,7 @@ int stitch_executor_create(const char* fused_graph_json, const char* options_jso
     if (o.has("colred")) opts.codegen.colred = o.at("colred").as_bool();
     if (o.has("row_prefetch_warp")) opts.codegen.row_prefetch_warp = o.at("row_prefetch_warp").as_bool();
     if (o.has("rcp_divide")) opts.codegen.rcp_divide = o.at("rcp_divide").as_bool();
+    if (o.has("gws")) opts.codegen.gws = o.at("gws").as_bool();
     if (o.has("tma_early")) opts.codegen.tma_early = o.at("tma_early").as_bool();
     if (o.has("cross_smem")) opts.codegen.cross_smem = o.at("cross_smem").as_bool();
     if (o.has("cross_smem_min_regs")) opts.codegen.cross_smem_min_regs = static_cast<int>(o.at("cross_smem_min_regs").as_int());

@@ -125,6 +125,8 @@ class Builder {
   KernelSpec build();
 
  private:
+  bool build_gws();  // the warp-specialised tcgen05 scheme, when the group fits it
+  bool nr_div_ = false;  // elementwise divides as branch-free rcp + Newton (gws tails)
   // ---- analysis ----
   void collect();
   std::vector<Component> components();
@@ -942,7 +944,8 @@ std::string Builder::elem_expr(const OpNode& op, const std::vector<std::string>&
     unsigned bits = 0;
     if (opts_.rcp_divide && std::sscanf(a[0].c_str(), "__int_as_float(0x%x)", &bits) == 1 && a[0].size() == 26 && (bits & 0x7fffffu) == 0 &&
         ((bits >> 23) & 0xffu) > 0 && ((bits >> 23) & 0xffu) < 0xffu)
-      return "(" + a[0] + " * __frcp_rn(" + a[1] + "))";
+      return "(" + a[0] + (nr_div_ ? " * stitch_dev::rcp_nr(" : " * __frcp_rn(") + a[1] + "))";
+    if (nr_div_) return "stitch_dev::div_nr(" + a[0] + ", " + a[1] + ")";
     return "(" + a[0] + " / " + a[1] + ")";
   }
   if (f == "maximum") return "fmaxf(" + a[0] + ", " + a[1] + ")";
@@ -979,6 +982,9 @@ std::string Builder::at(int v, const std::vector<std::string>& coords) {
     std::vector<std::string> args;
     if (x.node->elem_name == "broadcast") {
       args.push_back(at(x.operands[0], map_broadcast(x.operands[0], v, coords)));
+      // a broadcast literal stays a literal (constant folding downstream,
+      // e.g. c / x with c = 2^k as c * rcp(x))
+      if (args[0].rfind("__int_as_float(0x", 0) == 0 && args[0].size() == 26) return args[0];
     } else {
       for (int o : x.operands) args.push_back(at(o, coords));
     }
@@ -2186,9 +2192,210 @@ void Builder::emit_sectioned(const std::vector<int>& members) {
 // driver
 // ---------------------------------------------------------------------------
 
+
+// ---------------------------------------------------------------------------
+// GWS: warp-specialised tcgen05 batched-GEMM stage + generated tail
+// (device template stitch_dev::gws::run). Eligible fused groups: exactly two
+// batched dots over [S][64][64] whose four operands are kernel inputs of
+// that shape, every other member elementwise over [S][64][64] (broadcasts of
+// constants or inputs included), every output [S][64][64].
+// ---------------------------------------------------------------------------
+
+namespace {
+constexpr int kGwsThreads = 32 * (2 + 8 + 4 * 2);  // stitch_dev::gws::kThreads (STITCH_GWS_EPQ = 2)
+constexpr int kGwsElems = 16;                      // stitch_dev::gws::kElems
+constexpr int kGwsSmem = 3 * 65536 + 32768 + 8 * (2 * 3 + 9) + 16 + 1024;  // stitch_dev::gws::Smem::kAlloc
+}  // namespace
+
+bool Builder::build_gws() {
+  if (!opts_.gws || !opts_.allow_row) return false;
+  std::vector<int> dots;
+  int64_t S = -1;
+  auto tile = [&](int v) {
+    const auto& d = vals_[v].dims;
+    return d.size() == 3 && d[1] == 64 && d[2] == 64 && (S < 0 || d[0] == S);
+  };
+  for (int m : topo_members_) {
+    const OpNode& op = *vals_[m].node;
+    if (op.type == OpType::kBatchedDot) {
+      if (S < 0 && vals_[m].dims.size() == 3) S = vals_[m].dims[0];
+      if (!tile(m)) return false;
+      const auto& cd = op.contract_dims;
+      if (!(cd[0] < 0 || (cd[0] == 2 && cd[1] == 1))) return false;
+      for (int o : vals_[m].operands)
+        if (!vals_[o].external || !tile(o)) return false;
+      dots.push_back(m);
+    }
+  }
+  if (dots.size() != 2 || S < 1 || S > (1LL << 31) - 1) return false;
+  for (int m : topo_members_) {
+    const OpNode& op = *vals_[m].node;
+    if (op.type == OpType::kBatchedDot) continue;
+    if (op.type != OpType::kElementwise || !tile(m)) return false;
+  }
+  for (int o : outputs_)
+    if (!tile(o)) return false;
+  const int A0 = vals_[dots[0]].operands[0], B0 = vals_[dots[0]].operands[1];
+  const int A1 = vals_[dots[1]].operands[0], B1 = vals_[dots[1]].operands[1];
+  if (A0 == A1) return false;  // the stacked A' needs two tiles
+
+  // values the tail reads: dot results, staged A tiles, other full-tile
+  // inputs (prefetched one sample ahead), anything else through at()
+  std::set<int> tail_ext;  // full-tile external inputs read by the tail
+  int staged = 0;
+  for (int m : topo_members_) {
+    if (vals_[m].node->type == OpType::kBatchedDot) continue;
+    const bool bc = vals_[m].node->elem_name == "broadcast";
+    for (int o : vals_[m].operands) {
+      if (!vals_[o].external || bc || !tile(o)) continue;
+      if (o == A0) staged |= 1;
+      else if (o == A1) staged |= 2;
+      else tail_ext.insert(o);
+    }
+  }
+  std::map<int, std::string> argname;
+  for (int v : inputs_) argname[v] = in_ptr(v);
+
+  // ---- the tail functor
+  std::ostringstream& o = out_;
+  indent_ = 0;
+  ln("struct Tail {");
+  ++indent_;
+  for (int v : inputs_) ln("const float* __restrict__ " + in_ptr(v) + ";");
+  for (int v : outputs_) ln("float* __restrict__ " + out_ptr(v) + ";");
+  open("struct Regs");
+  for (int v : tail_ext) ln("float r" + std::to_string(v) + "[" + std::to_string(kGwsElems) + "];");
+  if (tail_ext.empty()) ln("int unused;");
+  close(";");
+  open("__device__ __forceinline__ void load(long long s, int q, int lane, int e, Regs& rg) const");
+  if (!tail_ext.empty()) {
+    ln("#pragma unroll");
+    open("for (int i = 0; i < " + std::to_string(kGwsElems) + "; i += 2)");
+    ln("const long long off = (s * 64 + stitch_dev::gws::elem_row(q, lane, i)) * 64 + stitch_dev::gws::elem_col(e, lane, i);");
+    for (int v : tail_ext) {
+      ln("{ const float2 t = __ldg(reinterpret_cast<const float2*>(" + in_ptr(v) + " + off)); rg.r" + std::to_string(v) +
+         "[i] = t.x; rg.r" + std::to_string(v) + "[i + 1] = t.y; }");
+    }
+    close();
+  } else {
+    ln("(void)s; (void)q; (void)lane; (void)e; (void)rg;");
+  }
+  close();
+  open("__device__ __forceinline__ void operator()(long long s, int q, int lane, int e, const float* d0, const float* d1, "
+       "const float* a0, const float* a1, const Regs& rg) const");
+  ln("(void)a0; (void)a1; (void)rg;");
+  ln("#pragma unroll");
+  open("for (int i = 0; i < " + std::to_string(kGwsElems) + "; i += 2)");
+  ln("const int row = stitch_dev::gws::elem_row(q, lane, i), col = stitch_dev::gws::elem_col(e, lane, i);");
+  ln("const long long off = (s * 64 + row) * 64 + col;");
+  for (int v : outputs_) ln("float o" + std::to_string(v) + "[2];");
+  ln("#pragma unroll");
+  open("for (int x = 0; x < 2; ++x)");
+  ln("const int ii = i + x, cc = col + x;");
+  ln("(void)ii; (void)cc;");
+  nr_div_ = true;
+  row_hook_ = [&](int v, const std::vector<std::string>& coords) -> std::string {
+    (void)coords;
+    if (v == dots[0]) return "d0[ii]";
+    if (v == dots[1]) return "d1[ii]";
+    if (v == A0 && (staged & 1)) return "a0[ii]";
+    if (v == A1 && (staged & 2)) return "a1[ii]";
+    if (tail_ext.count(v)) return "rg.r" + std::to_string(v) + "[ii]";
+    return "";
+  };
+  memo_.emplace_back();
+  for (int v : outputs_) {
+    std::string e = at(v, {"s", "row", "cc"});
+    ln("o" + std::to_string(v) + "[x] = " + e + ";");
+  }
+  memo_.pop_back();
+  row_hook_ = nullptr;
+  nr_div_ = false;
+  close();
+  for (int v : outputs_)
+    ln("*reinterpret_cast<float2*>(" + out_ptr(v) + " + off) = make_float2(o" + std::to_string(v) + "[0], o" +
+       std::to_string(v) + "[1]);");
+  close();
+  close();
+  --indent_;
+  ln("};");
+  std::string tail_src = o.str();
+  out_.str("");
+
+  // ---- signature: standard pointers, then the four tensor maps by value
+  std::vector<std::string> params;
+  auto input_index = [&](int v) {
+    return static_cast<int>(std::find(inputs_.begin(), inputs_.end(), v) - inputs_.begin());
+  };
+  for (int v : inputs_) {
+    params.push_back("const float* __restrict__ " + in_ptr(v));
+    spec_.inputs.push_back(vals_[v].id);
+    spec_.algo_bytes += vals_[v].node->shape.byte_count();
+  }
+  for (int v : outputs_) {
+    params.push_back("float* __restrict__ " + out_ptr(v));
+    spec_.outputs.push_back(vals_[v].id);
+    spec_.algo_bytes += vals_[v].node->shape.byte_count();
+  }
+  params.push_back("float* __restrict__ ws");
+  params.push_back("unsigned int* __restrict__ gsync");
+  params.push_back("const long long row_lo");
+  params.push_back("const long long row_hi");
+  const int ops[4] = {A0, A1, B0, B1};
+  for (int k = 0; k < 4; ++k) {
+    params.push_back("const __grid_constant__ stitch_dev::gws::TmaDesc tm" + std::to_string(k));
+    KernelSpec::TmaParam tp;
+    tp.input = input_index(ops[k]);
+    tp.box_rows = k < 2 ? 16 : 64;
+    tp.swizzle = k < 2 ? 0 : 1;
+    tp.samples = S;
+    spec_.tma.push_back(tp);
+  }
+  std::ostringstream head;
+  head << "// stitched kernel for fused op '" << name_ << "': " << topo_members_.size()
+       << " ops, scheme gws (warp-specialised tcgen05 3xTF32 batched-GEMM stage, " << S << " samples of 64x64)\n";
+  for (int m : topo_members_) {
+    head << "//   " << vals_[m].id << " = " << to_string(vals_[m].node->type);
+    if (!vals_[m].node->elem_name.empty()) head << ":" << vals_[m].node->elem_name;
+    head << "(";
+    for (size_t i = 0; i < vals_[m].operands.size(); ++i) head << (i ? ", " : "") << vals_[vals_[m].operands[i]].id;
+    head << ")\n";
+  }
+  head << tail_src;
+  head << "static_assert(stitch_dev::gws::kThreads == " << kGwsThreads << " && stitch_dev::gws::kElems == " << kGwsElems
+       << " && stitch_dev::gws::Smem::kAlloc == " << kGwsSmem << ", \"codegen / device gws constants\");\n";
+  head << "extern \"C\" __global__ void __launch_bounds__(" << kGwsThreads << ", 1) " << name_ << "(" << join(params, ", ")
+       << ") {\n";
+  head << "  extern __shared__ __align__(1024) unsigned char smem[];\n";
+  head << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
+  head << "  asm volatile(\"griddepcontrol.launch_dependents;\");\n";
+  head << "  (void)ws; (void)gsync; (void)row_lo; (void)row_hi;\n";
+  head << "  const Tail tail{";
+  {
+    std::vector<std::string> init;
+    for (int v : inputs_) init.push_back(in_ptr(v));
+    for (int v : outputs_) init.push_back(out_ptr(v));
+    head << join(init, ", ");
+  }
+  head << "};\n";
+  head << "  stitch_dev::gws::run<" << staged << ">(&tm0, &tm1, &tm2, &tm3, 0, " << S << "LL, smem, tail);\n";
+  head << "}\n";
+  spec_.source = head.str();
+  spec_.scheme = "gws(S=" + std::to_string(S) + ",tcgen05)";
+  spec_.composition = {"thread", "block", "tensor"};
+  spec_.block = kGwsThreads;
+  spec_.smem_bytes = kGwsSmem;
+  spec_.max_grid = static_cast<int>(std::min<int64_t>(S, 1 << 20));
+  spec_.flops = 2LL * 2 * 64 * 64 * 64 * S;
+  spec_.workspace_floats = 0;
+  spec_.sync_words = 0;
+  return true;
+}
+
 KernelSpec Builder::build() {
   collect();
   spec_.name = name_;
+  if (build_gws()) return spec_;
   std::vector<Component> comps = components();
   bool sectioned = false;
   for (Component& c : comps) {

@@ -53,6 +53,16 @@ struct KernelSpec {
   // them with any warp count <= block; shared memory scales per warp.
   bool flex_block = false;
   int min_grid = 1;                  // ranged packing: at least one CTA per component
+  // TMA tensor maps passed by value after the standard arguments (gws scheme):
+  // input argument index, box rows, 0 = 128B swizzle (K-major A operand),
+  // 1 = 128B swizzle of 32-byte atoms (MN-major B operand); [S][64][64] fp32
+  struct TmaParam {
+    int input = 0;
+    int box_rows = 64;
+    int swizzle = 0;
+    int64_t samples = 0;
+  };
+  std::vector<TmaParam> tma;
   int smem_per_warp = 0;
   int64_t rows = 0;
   int rows_per_cta = 1;
@@ -74,6 +84,10 @@ struct CodegenOptions {
   bool colred = true;
   bool colred_fused = true;
   bool rcp_divide = true;  // c / x with c = +-2^k as the exact c * rcp.rn(x)
+  // Row groups of [S][64][64] tiles with two batched dots on kernel inputs
+  // (the GRU group): the warp-specialised tcgen05 scheme (device gws::run,
+  // TMA producer / MMA issuer / split / tail warps). Off: the ROW scheme.
+  bool gws = true;
   bool tma_early = false;  // CTA rows: next row's TMA tiles requested as soon as their last reader is done
   bool cross_smem = true;  // warp rows: many column-reduction partials in the warp's shared slab
   int cross_smem_min_regs = 16;  // ... when they would take more than this many registers per lane

@@ -51,6 +51,7 @@ struct CudaApi {
   STITCH_CU_FN(cuGraphExecDestroy)
   STITCH_CU_FN(cuGraphDestroy)
   STITCH_CU_FN(cuGetErrorString)
+  STITCH_CU_FN(cuTensorMapEncodeTiled)
 #undef STITCH_CU_FN
 
   static CudaApi& get() {
@@ -107,6 +108,7 @@ struct CudaApi {
     STITCH_CU_LOAD(cuGraphExecDestroy, "cuGraphExecDestroy")
     STITCH_CU_LOAD(cuGraphDestroy, "cuGraphDestroy")
     STITCH_CU_LOAD(cuGetErrorString, "cuGetErrorString")
+    STITCH_CU_LOAD(cuTensorMapEncodeTiled, "cuTensorMapEncodeTiled")
 #undef STITCH_CU_LOAD
     return a;
   }

@@ -281,8 +281,14 @@ void Executor::build_kernels() {
     bufs_[it->second].kind = ValueBuf::kOutput;
     bufs_[it->second].slot = static_cast<int>(i);
   }
-  // Compile (or fetch from the cache).
+  // Compile (or fetch from the cache). STITCH_DUMP_DIR: also write every
+  // generated kernel body there as <name>.cu (inspection / profiling aid).
+  const char* dump = std::getenv("STITCH_DUMP_DIR");
   for (KernelInst& k : kernels_) {
+    if (dump && *dump) {
+      std::ofstream f(std::string(dump) + "/" + k.spec.name + ".cu");
+      f << k.spec.source;
+    }
     bool hit = false;
     std::string cubin = compile_cubin(full_source(k.spec), opts_.cache_dir, &hit);
     k.cache_hit = hit;
@@ -517,6 +523,29 @@ void Executor::launch_one(int i, int c, int chunks, const void* const* inputs, v
   }
   args[na] = &rng[0];
   args[na + 1] = &rng[1];
+  // gws scheme: tensor maps of the operand tiles, by value after row_lo/row_hi
+  if (!k.spec.tma.empty()) {
+    k.tmaps.resize(k.spec.tma.size());
+    k.tmap_ptrs.resize(k.spec.tma.size(), 0);
+    for (size_t t = 0; t < k.spec.tma.size(); ++t) {
+      const KernelSpec::TmaParam& tp = k.spec.tma[t];
+      const CUdeviceptr ptr = vals[tp.input];
+      if (k.tmap_ptrs[t] != ptr) {
+        cuuint64_t dims[3] = {64, 64, static_cast<cuuint64_t>(tp.samples)};
+        cuuint64_t strides[2] = {256, 16384};
+        cuuint32_t box[3] = {32, static_cast<cuuint32_t>(tp.box_rows), 1};
+        cuuint32_t es[3] = {1, 1, 1};
+        cu_check(cu.cuTensorMapEncodeTiled(reinterpret_cast<CUtensorMap*>(k.tmaps[t].v), CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                                           3, reinterpret_cast<void*>(ptr), dims, strides, box, es,
+                                           CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                           tp.swizzle ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE),
+                 "cuTensorMapEncodeTiled");
+        k.tmap_ptrs[t] = ptr;
+      }
+      args.push_back(k.tmaps[t].v);
+    }
+  }
   CUlaunchConfig cfg;
   std::memset(&cfg, 0, sizeof cfg);
   cfg.gridDimX = grid;

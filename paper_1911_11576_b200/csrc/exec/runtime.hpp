@@ -74,8 +74,16 @@ struct Segment {  // kernels [first, last] in launch order, run chunk by chunk w
   int first = 0, last = 0, chunks = 1;
 };
 
+struct alignas(64) TmapBytes {  // a CUtensorMap
+  unsigned long long v[16];
+};
+
 struct KernelInst {
   KernelSpec spec;
+  // gws scheme: TMA tensor maps encoded for the input pointers of the last
+  // launch, re-encoded when they change
+  std::vector<TmapBytes> tmaps;
+  std::vector<unsigned long long> tmap_ptrs;
   std::string op_id;                 // fused op or unfused op id in the fused graph
   std::vector<int> in_bufs, out_bufs;
   void* module = nullptr;            // CUmodule

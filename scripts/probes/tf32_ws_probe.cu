@@ -28,9 +28,9 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const TmaDesc* tm, int c0
       : "memory");
 }
 
-__device__ __forceinline__ u64 desc(u32 saddr, u32 lbo, u32 sbo) {
+__device__ __forceinline__ u64 desc(u32 saddr, u32 lbo, u32 sbo, u32 layout = 2) {
   return static_cast<u64>((saddr >> 4) & 0x3FFFu) | (static_cast<u64>((lbo >> 4) & 0x3FFFu) << 16) |
-         (static_cast<u64>((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (2ull << 61);
+         (static_cast<u64>((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (static_cast<u64>(layout) << 61);
 }
 // kind::tf32, D f32, M = 64, N = 64; b_major: 0 K-major, 1 MN-major
 __host__ __device__ constexpr u32 idesc(u32 b_major) {
@@ -62,7 +62,8 @@ __device__ void store_d(u32 tmem, float* out) {
 }
 
 __global__ void __launch_bounds__(128) probe(int mode, const __grid_constant__ TmaDesc tmA,
-                                             const __grid_constant__ TmaDesc tmB, float* out, u32* map) {
+                                             const __grid_constant__ TmaDesc tmB, float* out, u32* map,
+                                             u32 blbo, u32 bsbo, u32 bmajor) {
   extern __shared__ __align__(1024) unsigned char sm_raw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
   unsigned char* A = sm;             // 16 KB raw (2 k-boxes of 8 KB)
@@ -123,12 +124,20 @@ __global__ void __launch_bounds__(128) probe(int mode, const __grid_constant__ T
       for (int p = 0; p < 3; ++p)
         for (int kk = 0; kk < 8; ++kk)
           tc::mma_tf32(tmem, desc(smem_addr(as[p]) + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024),
-                       desc(smem_addr(bs[p]) + kk * 1024, 8192, 1024), idesc(1), (p | kk) != 0);
+                       bmajor == 2 ? desc(smem_addr(bs[p]) + kk * 1024, blbo, bsbo, 1)
+                       : bmajor ? desc(smem_addr(bs[p]) + kk * 1024, blbo, bsbo)
+                              : desc(smem_addr(bs[p]) + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024),
+                       idesc(bmajor ? 1 : 0), (p | kk) != 0);
       tc::commit(mbar);
     }
     mbar_wait(mbar, 0);
     tc::fence_after();
-    store_d(tmem, out);
+    if (bmajor == 7) {  // dump raw smem A then B
+      for (int i = t; i < 4096; i += blockDim.x) out[i] = reinterpret_cast<const float*>(A)[i];
+      for (int i = t; i < 4096; i += blockDim.x) out[4096 + i] = reinterpret_cast<const float*>(B)[i];
+    } else {
+      store_d(tmem, out);
+    }
   } else {
     // st 32x32b: TMEM lane L, column c holds L * 1000 + c; ld 16x256b.x1 at
     // lane base 32w, column 0: record what each thread got
@@ -156,7 +165,7 @@ __global__ void __launch_bounds__(128) probe(int mode, const __grid_constant__ T
   tc::dealloc(tmem, 64);
 }
 
-static TmaDesc make_map(CUdeviceptr base, int batch) {
+static TmaDesc make_map(CUdeviceptr base, int batch, CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B) {
   TmaDesc d;
   cuuint64_t dims[3] = {64, 64, (cuuint64_t)batch};
   cuuint64_t strides[2] = {256, 16384};
@@ -164,7 +173,7 @@ static TmaDesc make_map(CUdeviceptr base, int batch) {
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = cuTensorMapEncodeTiled(reinterpret_cast<CUtensorMap*>(&d), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
                                       reinterpret_cast<void*>(base), dims, strides, box, es,
-                                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                      CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     printf("tensor map encode failed %d\n", (int)r);
@@ -189,7 +198,7 @@ int main() {
   TmaDesc tA = make_map((CUdeviceptr)dA, 1), tB = make_map((CUdeviceptr)dB, 1);
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 70000);
   // mode 0
-  probe<<<1, 128, 70000>>>(0, tA, tB, dOut, dMap);
+  probe<<<1, 128, 70000>>>(0, tA, tB, dOut, dMap, 0, 0, 0);
   if (cudaDeviceSynchronize() != cudaSuccess) { printf("mode0 failed: %s\n", cudaGetErrorString(cudaGetLastError())); return 1; }
   cudaMemcpy(out.data(), dOut, 16384, cudaMemcpyDeviceToHost);
   int trunc_ok = 0, rn_ok = 0;
@@ -201,31 +210,70 @@ int main() {
   }
   printf("mode0 tf32 operand conversion: matches truncation %d/64, round-to-nearest %d/64  (D[7][5]=%.9g)\n", trunc_ok,
          rn_ok, out[7 * 64 + 5]);
-  // mode 1
-  probe<<<1, 128, 70000>>>(1, tA, tB, dOut, dMap);
-  if (cudaDeviceSynchronize() != cudaSuccess) { printf("mode1 failed: %s\n", cudaGetErrorString(cudaGetLastError())); return 1; }
-  cudaMemcpy(out.data(), dOut, 16384, cudaMemcpyDeviceToHost);
-  double worst = 0, maxerr = 0;
-  for (int m = 0; m < 64; ++m)
-    for (int n = 0; n < 64; ++n) {
-      double ref = 0, ab = 0;
+  // mode 1 variants: (lbo, sbo, b_major); b_major 7 = dump smem after TMA
+  std::vector<float> big(8192);
+  cudaMalloc(&dOut, 32768);
+  probe<<<1, 128, 70000>>>(1, tA, tB, dOut, dMap, 0, 0, 7);
+  if (cudaDeviceSynchronize() != cudaSuccess) { printf("dump failed\n"); return 1; }
+  cudaMemcpy(big.data(), dOut, 32768, cudaMemcpyDeviceToHost);
+  {
+    // expected SW128 placement of A[m][k] (box kb = k/32): kb*2048 + m*32 + ((k%32/4) ^ (m%8))*4 + k%4 (floats)
+    int okA = 0, okB = 0;
+    for (int m = 0; m < 64; ++m)
       for (int k = 0; k < 64; ++k) {
-        ref += (double)A[m * 64 + k] * B[k * 64 + n];
-        ab += std::fabs((double)A[m * 64 + k] * B[k * 64 + n]);
+        const int kb = k / 32, kc = (k % 32) / 4;
+        const int off = kb * 2048 + m * 32 + ((kc ^ (m % 8)) * 4) + k % 4;
+        okA += big[off] == A[m * 64 + k];
+        okB += big[4096 + off] == B[m * 64 + k];
       }
-      const double e = std::fabs(out[m * 64 + n] - ref);
-      maxerr = std::max(maxerr, e);
-      worst = std::max(worst, e / (64 * std::ldexp(1.0, -24) * ab));
+    printf("TMA dump: A matches SW128 placement %d/4096, B %d/4096; A[0]=%g smem[0]=%g\n", okA, okB, A[0], big[0]);
+  }
+  // B loaded with the 128B swizzle of 32-byte atoms: dump and decode
+  TmaDesc tB32 = make_map((CUdeviceptr)dB, 1, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  probe<<<1, 128, 70000>>>(1, tA, tB32, dOut, dMap, 0, 0, 7);
+  cudaDeviceSynchronize();
+  cudaMemcpy(big.data(), dOut, 32768, cudaMemcpyDeviceToHost);
+  printf("ATOM_32B dump, rows 0..8 (k), element position of B[k][n] for n = 0,4,8,...,28 (in floats within the row):\n");
+  for (int k = 0; k < 9; ++k) {
+    printf("  k=%d:", k);
+    for (int n = 0; n < 32; n += 4) {
+      int pos = -1;
+      for (int q = 0; q < 32; ++q)
+        if (big[4096 + k * 32 + q] == B[k * 64 + n]) pos = q;
+      printf(" %2d", pos);
     }
-  printf("mode1 TMA + MN-major B 3xTF32: max abs err %.3g, worst err / (K u sum|ab|) %.3g  D[0][0]=%.6f\n", maxerr, worst,
-         out[0]);
+    printf("\n");
+  }
+  tB = tB32;
+  const unsigned variants[][3] = {{8192, 512, 2}, {8192, 1024, 2}, {512, 8192, 2}, {1024, 8192, 2}, {8192, 256, 2}};
+  for (auto& v : variants) {
+    probe<<<1, 128, 70000>>>(1, tA, tB, dOut, dMap, v[0], v[1], v[2]);
+    if (cudaDeviceSynchronize() != cudaSuccess) { printf("mode1 failed: %s\n", cudaGetErrorString(cudaGetLastError())); return 1; }
+    cudaMemcpy(out.data(), dOut, 16384, cudaMemcpyDeviceToHost);
+    double worst = 0, maxerr = 0, worstT = 0;
+    for (int m = 0; m < 64; ++m)
+      for (int n = 0; n < 64; ++n) {
+        double ref = 0, ab = 0, refT = 0;
+        for (int k = 0; k < 64; ++k) {
+          ref += (double)A[m * 64 + k] * B[k * 64 + n];
+          refT += (double)A[m * 64 + k] * B[n * 64 + k];
+          ab += std::fabs((double)A[m * 64 + k] * B[k * 64 + n]);
+        }
+        const double e = std::fabs(out[m * 64 + n] - ref);
+        maxerr = std::max(maxerr, e);
+        worst = std::max(worst, e / (64 * std::ldexp(1.0, -24) * ab));
+        worstT = std::max(worstT, std::fabs(out[m * 64 + n] - refT));
+      }
+    printf("mode1 lbo=%u sbo=%u b_major=%u: max abs err %.3g (vs A.B^T %.3g), worst err/(K u sum|ab|) %.3g, D[0][0]=%.6f D[5][40]=%.6f\n",
+           v[0], v[1], v[2], maxerr, worstT, worst, out[0], out[5 * 64 + 40]);
+  }
   // mode 2
-  probe<<<1, 128, 70000>>>(2, tA, tB, dOut, dMap);
+  probe<<<1, 128, 70000>>>(2, tA, tB, dOut, dMap, 0, 0, 0);
   if (cudaDeviceSynchronize() != cudaSuccess) { printf("mode2 failed: %s\n", cudaGetErrorString(cudaGetLastError())); return 1; }
   std::vector<u32> map(512);
   cudaMemcpy(map.data(), dMap, 512 * 4, cudaMemcpyDeviceToHost);
   printf("mode2 16x256b.x1 fragment (warp 0): thread: reg -> (lane, col)\n");
-  for (int t = 0; t < 32; ++t) {
+  for (int t = 0; t < 4; ++t) {
     printf("  t%02d:", t);
     for (int j = 0; j < 4; ++j) printf(" (%u,%u)", map[t * 4 + j] / 1000, map[t * 4 + j] % 1000);
     printf("\n");

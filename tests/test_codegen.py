@@ -38,9 +38,33 @@ def test_expected_schemes():
     (k,) = ex.info["kernels"]
     assert k["scheme"].startswith("row_warp") and {"thread", "warp"} <= set(k["composition"])
     g = W.gru()
-    ex = compile_only(rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT)["fused"])
-    (k,) = ex.info["kernels"]
+    fused = rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT)["fused"]
+    (k,) = compile_only(fused).info["kernels"]
+    # the warp-specialised tcgen05 scheme by default, the FFMA ROW scheme without it
+    assert k["scheme"].startswith("gws") and "tensor" in k["composition"] and k["flops"] == 2 * 2 * 4096 * 64 ** 3
+    assert k["block"] == 576 and k["smem_bytes"] == 230536
+    (k,) = compile_only(fused, gws=False).info["kernels"]
     assert "row_cta" in k["scheme"] and "block" in k["composition"] and k["flops"] == 2 * 2 * 4096 * 64 ** 3
+
+
+def test_gws_kernel_source_shape():
+    """The generated gws kernel: four tensor maps by value, the device
+    template with the A0 tile staged for the tail (z * h), branch-free
+    power-of-two divides, and the tensor-map parameters the runtime encodes."""
+    import os
+    import tempfile
+    g = W.gru(batch=300)
+    fused = rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT)["fused"]
+    d = tempfile.mkdtemp()
+    os.environ["STITCH_DUMP_DIR"] = d
+    try:
+        compile_only(fused)
+    finally:
+        del os.environ["STITCH_DUMP_DIR"]
+    src = open(os.path.join(d, "fusion_0.cu")).read()
+    assert src.count("__grid_constant__ stitch_dev::gws::TmaDesc") == 4
+    assert "stitch_dev::gws::run<1>(&tm0, &tm1, &tm2, &tm3, 0, 300LL, smem, tail)" in src
+    assert "stitch_dev::rcp_nr(" in src and " / " not in src.split("struct Tail")[1].split("static_assert")[0]
 
 
 @pytest.mark.parametrize("name", list(W.CONFIGS))

@@ -208,12 +208,13 @@ def test_gru_double_buffer_and_prefetch_variants():
     g = W.gru(batch=37, n=64)
     fused = rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT)["fused"]
     ins = orc.random_inputs(g, seed=52)
-    ex = assert_parity(g, fused, ins, tma_double_buffer=True, row_prefetch=True)
+    ex = assert_parity(g, fused, ins, tma_double_buffer=True, row_prefetch=True, gws=False)
     assert "tma2" in ex.info["kernels"][0]["scheme"]
 
 
 VARIANTS = [dict(pack_sequential=True), dict(loop_fusion=False), dict(row_prefetch=False), dict(row_prefetch_warp=True),
-            dict(tma_double_buffer=True), dict(tensor_cores=True), dict(colred=False), dict(lazy_inputs=True),
+            dict(tma_double_buffer=True), dict(tensor_cores=True, gws=False), dict(colred=False), dict(lazy_inputs=True),
+            dict(gws=False), dict(gws=False, tma_double_buffer=True),
             dict(pdl=False), dict(fold_constants=False), dict(colred_cp_async=False), dict(colred_cols=128), dict(cross_smem=False), dict(tma_early=True)]
 
 
@@ -234,8 +235,8 @@ def test_gru_tensor_core_gemm_stage(batch):
     stitched GRU group matches the oracle within the fp32 dot bound."""
     g = W.gru(batch=batch, n=64)
     fused = rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT)["fused"]
-    for opts in (dict(tensor_cores=True), dict(tensor_cores=True, tc_pipeline=False),
-                 dict(tensor_cores=True, tc_direct_loads=True)):
+    for opts in (dict(tensor_cores=True, gws=False), dict(tensor_cores=True, tc_pipeline=False, gws=False),
+                 dict(tensor_cores=True, tc_direct_loads=True, gws=False)):
         ex = assert_parity(g, fused, orc.random_inputs(g, seed=71), **opts)
         assert "tcgen05" in ex.info["kernels"][0]["scheme"] and "tensor" in ex.info["kernels"][0]["composition"]
 
@@ -462,3 +463,62 @@ def test_executor_uses_its_own_device_context():
     ref, bound = tolerance.reference_with_bound(g, ins)
     for o, r, b in zip(host_out, ref, bound):
         assert tolerance.check(o, r, b)[0]
+
+
+def _gru_like(S, extra=False):
+    """The GRU cell; with extra=True also a broadcast bias [64] in the
+    pre-activation and a second full-tile input y in the output (the gws
+    tail's broadcast and prefetched-input paths)."""
+    if not extra:
+        return W.gru(batch=S, n=64)
+    g = W.GraphBuilder()
+    full = [S, 64, 64]
+    h, Wt, x, U, y = (g.param(n, full) for n in ("h", "W", "x", "U", "y"))
+    bias = g.param("bias", [64])
+    hw = g.bdot("hw", h, Wt, full)
+    xu = g.bdot("xu", x, U, full)
+    pre = g.ew("pre", "add", [hw, xu], full)
+    pb = g.ew("pb", "add", [pre, g.bcast("bias_b", bias, full)], full)
+    one = g.bcast("one_b", g.const("one", 1.0), full)
+    e = g.ew("e", "exp", [g.ew("npb", "negate", [pb], full)], full)
+    z = g.ew("z", "divide", [one, g.ew("d", "add", [one, e], full)], full)
+    q = g.ew("q", "divide", [y, g.ew("d2", "add", [one, g.ew("zz", "multiply", [z, z], full)], full)], full)
+    out = g.ew("out", "add", [g.ew("zh", "multiply", [z, h], full), q], full)
+    return g.graph([g.ew("t", "subtract", [out, x], full)])
+
+
+@pytest.mark.parametrize("S", [1, 37, 148, 149, 300])
+@pytest.mark.parametrize("extra", [False, True])
+def test_gws_tcgen05_parity(S, extra):
+    """The warp-specialised tcgen05 scheme (TMA producer, MMA issuer, split
+    and tail warps; 3xTF32) on sample counts below, at and above the grid,
+    against the oracle and against the FFMA ROW scheme."""
+    g = _gru_like(S, extra)
+    fused = rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT)["fused"]
+    ins = orc.random_inputs(g, seed=70 + S)
+    ex = assert_parity(g, fused, ins)
+    assert any(k["scheme"].startswith("gws") for k in ex.info["kernels"]), ex.info["kernels"]
+    _, a = run_device(fused, ins)
+    _, b = run_device(fused, ins, gws=False)
+    ref, bound = tolerance.reference_with_bound(g, ins)
+    for x, y, r, bd in zip(a, b, ref, bound):
+        # both schemes sit within tolerance of the fp64 value: within the sum of both of each other
+        tol = 2 * (np.maximum(tolerance.RTOL * np.abs(r), tolerance.ATOL) + tolerance.SAFETY * bd)
+        assert (np.abs(x.astype(np.float64) - y) <= tol).all()
+
+
+def test_gws_launch_list_and_replay():
+    """Graph replay with new pointers re-encodes the tensor maps."""
+    g = W.gru(batch=64)
+    fused = rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT)["fused"]
+    ex = rt.Executor(fused, device=0)
+    s = torch.cuda.current_stream().cuda_stream
+    for seed in (80, 81):
+        ins = orc.random_inputs(g, seed=seed)
+        d_in = [torch.from_numpy(np.ascontiguousarray(ins[i])).cuda() for i in ex.input_ids]
+        d_out = [torch.full(t["dims"], float("nan"), device="cuda") for t in ex.info["outputs"]]
+        ex.run(d_in, d_out, stream=s)
+        ex.run(d_in, d_out, stream=s)
+        torch.cuda.synchronize()
+        ref, bound = tolerance.reference_with_bound(g, ins)
+        assert tolerance.check(d_out[0].cpu().numpy(), ref[0], bound[0])[0]
