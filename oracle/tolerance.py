@@ -221,3 +221,38 @@ def check(got, ref, bound):
     ratio = np.where(np.isnan(ratio), np.inf, ratio)
     worst = float(ratio.max()) if ratio.size else 0.0
     return worst <= 1.0, worst
+
+
+def anchored_graph(graph, anchors):
+    """`graph` with every anchor value's CONSUMERS reading a parameter
+    "<id>@anchor" instead of the anchor itself; the anchor keeps its own
+    definition (it is still checked, from its own anchored operands)."""
+    nodes = []
+    for n in graph["nodes"]:
+        m = dict(n)
+        if "operands" in n:
+            m["operands"] = [o + "@anchor" if o in anchors else o for o in n["operands"]]
+        nodes.append(m)
+    shapes = {n["id"]: n["shape"] for n in graph["nodes"]}
+    extra = [{"id": a + "@anchor", "kind": "parameter", "shape": shapes[a]} for a in sorted(anchors)]
+    return {"nodes": extra + nodes, "outputs": list(graph["outputs"])}
+
+
+def anchored_reference_with_bound(graph, inputs, got):
+    """Step-wise certification for deep graphs (12-layer BERT): every graph
+    output that other nodes consume is an anchor; its consumers are
+    evaluated from the checked executor's value of it (`got[id]`, fp32), so
+    each output's fp64 reference and first-order bound cover only the ops
+    since the nearest anchors -- one layer, forward or backward -- instead of
+    the whole chain, whose worst-case bound is infinite after 12 LayerNorm
+    layers. Anchors are themselves outputs and are checked the same way from
+    their own anchors, so every output is certified against the ops between
+    two checked values. Returns (outputs, bounds) like reference_with_bound."""
+    outs = orc.graph_outputs(graph)
+    consumed = {o for n in graph["nodes"] for o in n.get("operands", [])}
+    anchors = {o for o in outs if o in consumed}
+    g2 = anchored_graph(graph, anchors)
+    ins2 = dict(inputs)
+    for a in anchors:
+        ins2[a + "@anchor"] = np.asarray(got[a], dtype=np.float32)
+    return reference_with_bound(g2, ins2)

@@ -98,6 +98,33 @@ std::string compile_cubin(const std::string& source, const std::string& cache_di
 
 // ---------------------------------------------------------------------------
 
+void apply_codegen_options(CodegenOptions& c, const json::Value& o) {
+  if (o.has("smem_limit_bytes")) c.max_smem = static_cast<int>(o.at("smem_limit_bytes").as_int());
+  if (o.has("allow_row")) c.allow_row = o.at("allow_row").as_bool();
+  if (o.has("num_sms")) c.num_sms = static_cast<int>(o.at("num_sms").as_int());
+  if (o.has("tc_pipeline")) c.tc_pipeline = o.at("tc_pipeline").as_bool();
+  if (o.has("tc_direct_loads")) c.tc_direct_loads = o.at("tc_direct_loads").as_bool();
+  if (o.has("tensor_cores")) c.tensor_cores = o.at("tensor_cores").as_bool();
+  if (o.has("pack_sequential")) c.pack_sequential = o.at("pack_sequential").as_bool();
+  if (o.has("wide_cross_threads")) c.wide_cross_threads = static_cast<int>(o.at("wide_cross_threads").as_int());
+  if (o.has("wide_cross_cta")) c.wide_cross_cta = o.at("wide_cross_cta").as_bool();
+  if (o.has("lazy_inputs")) c.lazy_inputs = o.at("lazy_inputs").as_bool();
+  if (o.has("colred")) c.colred = o.at("colred").as_bool();
+  if (o.has("row_prefetch_warp")) c.row_prefetch_warp = o.at("row_prefetch_warp").as_bool();
+  if (o.has("rcp_divide")) c.rcp_divide = o.at("rcp_divide").as_bool();
+  if (o.has("gws")) c.gws = o.at("gws").as_bool();
+  if (o.has("tma_early")) c.tma_early = o.at("tma_early").as_bool();
+  if (o.has("cross_smem")) c.cross_smem = o.at("cross_smem").as_bool();
+  if (o.has("cross_smem_min_regs")) c.cross_smem_min_regs = static_cast<int>(o.at("cross_smem_min_regs").as_int());
+  if (o.has("colred_fused")) c.colred_fused = o.at("colred_fused").as_bool();
+  if (o.has("colred_cp_async")) c.colred_cp_async = o.at("colred_cp_async").as_bool();
+  if (o.has("colred_cols")) c.colred_cols = static_cast<int>(o.at("colred_cols").as_int());
+  if (o.has("colred_ctas_per_sm")) c.colred_ctas_per_sm = static_cast<int>(o.at("colred_ctas_per_sm").as_int());
+  if (o.has("loop_fusion")) c.loop_fusion = o.at("loop_fusion").as_bool();
+  if (o.has("row_prefetch")) c.row_prefetch = o.at("row_prefetch").as_bool();
+  if (o.has("tma_double_buffer")) c.tma_double_buffer = o.at("tma_double_buffer").as_bool();
+}
+
 Executor::Executor(const Graph& fused, const ExecOptions& opts) : g_(fused), opts_(opts) {
   for (const OpNode& n : g_.nodes)
     if (n.type == OpType::kParameter || (n.type == OpType::kConstant && !n.value)) {
@@ -187,12 +214,27 @@ void Executor::build_kernels() {
              uniform.count(n.operands.at(0)))
       uniform[id] = uniform[n.operands[0]];
   }
+  // Broadcast sinking: top-level (unfused) broadcasts of small tensors.
+  std::map<std::string, std::string> sink_src;  // broadcast id -> its source
+  if (opts_.sink_broadcasts)
+    for (const std::string& id : topo) {
+      const OpNode& n = g_.at(id);
+      if (n.type != OpType::kElementwise || n.elem_name != "broadcast" || uniform.count(id)) continue;
+      const OpNode& src = g_.at(n.operands.at(0));
+      if (src.type == OpType::kTuple || src.type == OpType::kFused) continue;
+      if (src.shape.byte_count() <= opts_.sink_max_bytes && src.shape.byte_count() * 4 <= n.shape.byte_count())
+        sink_src[id] = n.operands[0];
+    }
   std::map<std::string, std::string> names;
   for (const std::string& id : topo) {
     const OpNode& n = g_.at(id);
     if (n.type != OpType::kFused && !is_fusible(n)) continue;
     if (n.type != OpType::kFused && uniform.count(id) && !graph_outs.count(id)) {
       ++folded_kernels_;
+      continue;
+    }
+    if (sink_src.count(id) && !graph_outs.count(id)) {
+      ++sunk_kernels_;  // every consumer kernel recomputes it from the source
       continue;
     }
     Graph body;
@@ -226,6 +268,58 @@ void Executor::build_kernels() {
       body.outputs = {"__outputs"};
       out_keys.push_back(id);
     }
+    // Sink broadcasts into this body: a parameter fed by a sunk broadcast
+    // becomes that broadcast over a parameter of its (small) source.
+    bool sinks = false;
+    {
+      int q = 0;
+      for (const OpNode& bn : body.nodes)
+        if (bn.type == OpType::kParameter) sinks = sinks || sink_src.count(outer_inputs.at(q++));
+    }
+    if (sinks) {
+      Graph nb;
+      std::vector<std::string> nouter;
+      std::map<std::string, std::string> param_of;  // outer value -> body parameter id
+      std::vector<std::pair<const OpNode*, std::string>> conv;  // body param node, source outer id
+      int q = 0;
+      for (const OpNode& bn : body.nodes) {
+        if (bn.type != OpType::kParameter) continue;
+        const std::string& outer = outer_inputs.at(q++);
+        auto it = sink_src.find(outer);
+        if (it != sink_src.end()) {
+          conv.push_back({&bn, it->second});
+        } else {
+          nb.add(bn);
+          nouter.push_back(outer);
+          param_of[outer] = bn.id;
+        }
+      }
+      for (auto& [bn, src] : conv) {
+        if (param_of.count(src)) continue;
+        OpNode prm;
+        prm.id = src + "__sunk";
+        while (body.contains(prm.id) || nb.contains(prm.id)) prm.id += "_";
+        prm.type = OpType::kParameter;
+        prm.shape = g_.at(src).shape;
+        nb.add(prm);
+        nouter.push_back(src);
+        param_of[src] = prm.id;
+      }
+      for (auto& [bn, src] : conv) {
+        OpNode b;
+        b.id = bn->id;
+        b.type = OpType::kElementwise;
+        b.elem_name = "broadcast";
+        b.operands = {param_of.at(src)};
+        b.shape = bn->shape;
+        nb.add(b);
+      }
+      for (const OpNode& bn : body.nodes)
+        if (bn.type != OpType::kParameter) nb.add(bn);
+      nb.outputs = body.outputs;
+      body = std::move(nb);
+      outer_inputs = std::move(nouter);
+    }
     // Body parameter id -> outer value (positional for fused bodies).
     std::map<std::string, std::string> outer_of;
     std::map<std::string, double> consts;
@@ -242,7 +336,13 @@ void Executor::build_kernels() {
     names[kname] = id;
     KernelInst k;
     k.op_id = id;
-    k.spec = generate_kernel(body, kname, consts, opts_.codegen);
+    // per-group codegen variant (Alg. 3 KernelEvalUpdate's measured choice)
+    CodegenOptions co = opts_.codegen;
+    if (opts_.kernel_options.is_object() && opts_.kernel_options.has(id)) {
+      apply_codegen_options(co, opts_.kernel_options.at(id));
+      k.variant = opts_.kernel_options.at(id);
+    }
+    k.spec = generate_kernel(body, kname, consts, co);
     const OpNode& tup = body.at(body.outputs.front());
     for (const std::string& in : k.spec.inputs) {
       const std::string& outer = outer_of.at(in);
@@ -849,6 +949,7 @@ json::Value Executor::describe() const {
     e.set("name", k.spec.name);
     e.set("op", k.op_id);
     e.set("scheme", k.spec.scheme);
+    e.set("variant", k.variant);
     json::Value comp = json::Value::array();
     for (const std::string& c : k.spec.composition) comp.push(c);
     e.set("composition", comp);
@@ -879,6 +980,7 @@ json::Value Executor::describe() const {
   j.set("schedule", sched);
   j.set("launches", launches_per_run_);
   j.set("folded_constant_kernels", folded_kernels_);
+  j.set("sunk_broadcast_kernels", sunk_kernels_);
   j.set("algo_bytes", algo);
   j.set("arena_bytes", arena_bytes_);
   j.set("workspace_bytes", ws_floats_ * 4);

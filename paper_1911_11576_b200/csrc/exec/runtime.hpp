@@ -46,11 +46,22 @@ struct ExecOptions {
   // broadcasts of constants left unfused by the plan are folded into their
   // consumers as literals instead of being materialised by a kernel
   bool fold_constants = true;
+  // Unfused broadcasts of small tensors (LayerNorm gamma/beta [H] ->
+  // [T, H]) are not materialised: each consumer kernel reads the source
+  // through the broadcast map instead (the broadcast moves into its body).
+  bool sink_broadcasts = true;
+  int64_t sink_max_bytes = 1 << 20;
   // programmatic dependent launch between consecutive (non-cooperative) kernels
   bool pdl = true;
   int chunk_ring = 2;
   CodegenOptions codegen;
+  // per fused-op codegen overrides {op id: {option: value}} (the measured
+  // per-group variant table, paper Alg. 3 KernelEvalUpdate)
+  json::Value kernel_options = json::Value::object();
 };
+
+// Codegen options from an options JSON object (keys as in stitch_executor_create).
+void apply_codegen_options(CodegenOptions& c, const json::Value& o);
 
 const std::string& device_header_source();
 std::string full_source(const KernelSpec& spec);
@@ -80,6 +91,7 @@ struct alignas(64) TmapBytes {  // a CUtensorMap
 
 struct KernelInst {
   KernelSpec spec;
+  json::Value variant = json::Value::object();  // per-group codegen overrides applied
   // gws scheme: TMA tensor maps encoded for the input pointers of the last
   // launch, re-encoded when they change
   std::vector<TmapBytes> tmaps;
@@ -128,6 +140,7 @@ class Executor {
   std::vector<Segment> segments_;
   int launches_per_run_ = 0;
   int folded_kernels_ = 0;
+  int sunk_kernels_ = 0;
   std::vector<void*> lanes_;        // CUstreams for pipelined chunk lanes
   std::vector<void*> lane_events_;  // CUevents: [segment-local kernel j][chunk c] done, plus fork/join
   void* copy_streams_[2] = {nullptr, nullptr};  // run_host: H2D and D2H copy streams

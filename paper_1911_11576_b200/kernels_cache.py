@@ -31,6 +31,9 @@ def plans(full=True, small=True):
                 for lim_tag, lim in (("b200", W.B200_SHARED_LIMIT), ("ref48k", W.REFERENCE_SHARED_LIMIT)):
                     out.append(("%s/%s/%s" % (name, size, lim_tag), rt.plan(g, shared_limit_bytes=lim)["fused"]))
             out.append(("%s/%s/unfused" % (name, size), g))
+    if full:
+        # tests/test_executor_gpu.py: the bench BERT plan's groups at a 1024-token batch
+        out.append(("bert/batch8/bench-groups", tuning.plan_like("bert", W.bert(batch=8))))
     return out
 
 
@@ -43,6 +46,42 @@ def _compile(args):
     return n, hits
 
 
+def variant_jobs(configs=None):
+    """(fused graph json, options) for every candidate of scripts/tune_variants.py."""
+    import importlib.util
+    import json
+    import os
+    spec = importlib.util.spec_from_file_location(
+        "tv", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts", "tune_variants.py"))
+    tv = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(tv)
+    jobs = []
+    for name in configs or list(W.CONFIGS):
+        fused = json.dumps(tuning.config_plan(name)[0]["fused"])
+        for v in tv.VARIANTS:
+            jobs.append((fused, dict(v)))
+    return jobs
+
+
+def prebuild_variants(configs=None, workers=None):
+    """Compile every tuning candidate (run before scripts/tune_variants.py on the box)."""
+    import concurrent.futures as cf
+    import os
+    n = hits = 0
+    with cf.ProcessPoolExecutor(workers or max(1, min(16, os.cpu_count() or 1))) as pool:
+        for a, b in pool.map(_compile_safe, variant_jobs(configs)):
+            n += a
+            hits += b
+    print("variant kernels: %d (%d already cached)" % (n, hits))
+
+
+def _compile_safe(args):
+    try:
+        return _compile(args)
+    except Exception:  # a variant that does not apply to a plan
+        return 0, 0
+
+
 def prebuild(verbose=True, workers=None):
     import concurrent.futures as cf
     import json
@@ -50,6 +89,8 @@ def prebuild(verbose=True, workers=None):
     jobs = []
     for tag, fused in plans():
         opts = {"chunking": False, "fold_constants": False} if tag.endswith("/unfused") else {}
+        if tag.endswith("/bench"):
+            opts["kernel_options"] = tuning.kernel_variants(tag.split("/")[0])
         jobs.append((json.dumps(fused), opts))
     n = hits = 0
     with cf.ProcessPoolExecutor(workers or max(1, min(16, os.cpu_count() or 1))) as pool:

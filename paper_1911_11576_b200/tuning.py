@@ -162,6 +162,33 @@ def cached_plan(name, graph, options):
     return d["result"]
 
 
+def kernel_variants(name):
+    """The measured per-group codegen variant table of suite config `name`
+    (data/kernel_variants/<name>.json, scripts/tune_variants.py): {op id:
+    codegen overrides}, passed to the executor as kernel_options; {} when
+    none is shipped."""
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "data", "kernel_variants", name + ".json")
+    if not os.path.exists(p):
+        return {}
+    with open(p) as f:
+        return json.load(f)["table"]
+
+
+def groups_of(fused):
+    """The fusion groups (op ids per fused node) of a fused graph."""
+    return [[m["id"] for m in n["body"]["nodes"] if m["kind"] not in ("parameter", "tuple", "constant")]
+            for n in fused["nodes"] if n["kind"] == "fused"]
+
+
+def plan_like(name, graph):
+    """`graph` (the config at another batch size: op ids do not depend on it)
+    fused with exactly the groups of the plan bench.py runs for `name` --
+    e.g. the shipped 12-layer BERT plan at a batch the oracle can check."""
+    fused = config_plan(name)[0]["fused"]
+    pats = groups_of(fused)
+    return rt.debug_call("apply_plan", graph=graph, patterns=pats, selected=list(range(len(pats))))["graph"]
+
+
 def config_plan(name, graph=None, shared_limit_bytes=None):
     """The plan bench.py runs for suite config `name`: execution-based scores
     from the shipped B200 table when `graph` is the config at its BASELINE

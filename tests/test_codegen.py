@@ -106,3 +106,29 @@ def test_colred_output_feeding_post_op_compiles():
     fused = rt.plan(g)["fused"]
     assert sum(n["kind"] == "fused" for n in fused["nodes"]) == 1
     compile_only(fused)
+
+
+def test_broadcast_sinking():
+    """Unfused broadcasts of small tensors are not materialised: the BERT
+    bench plan's LayerNorm gamma broadcasts move into their consumers'
+    bodies (fewer kernels, fewer bytes), and a graph output broadcast still
+    gets its kernel."""
+    from paper_1911_11576_b200 import tuning
+    f = tuning.config_plan("bert", W.bert())[0]["fused"]
+    on = compile_only(f).info
+    off = compile_only(f, sink_broadcasts=False).info
+    assert on["sunk_broadcast_kernels"] >= 10
+    assert len(on["kernels"]) == len(off["kernels"]) - on["sunk_broadcast_kernels"]
+    assert on["algo_bytes"] < off["algo_bytes"]
+    R, C = 256, 64
+    g = {"nodes": [_node("x", "parameter", dims=(R, C)), _node("gam", "parameter", dims=(C,)),
+                   _node("gb", "elementwise", ["gam"], "broadcast", dims=(R, C)),
+                   _node("y", "elementwise", ["x", "gb"], "multiply", dims=(R, C)),
+                   _node("z", "elementwise", ["gb", "x"], "add", dims=(R, C)),
+                   {"id": "t", "kind": "tuple", "operands": ["y", "z"], "shape": {"dims": [R, C], "dtype": "f32"}}],
+         "outputs": ["t"]}
+    info = compile_only(g).info
+    assert info["sunk_broadcast_kernels"] == 1 and len(info["kernels"]) == 2
+    g["nodes"][-1]["operands"] = ["y", "z", "gb"]
+    info = compile_only(g).info
+    assert info["sunk_broadcast_kernels"] == 0 and len(info["kernels"]) == 3

@@ -522,3 +522,57 @@ def test_gws_launch_list_and_replay():
         torch.cuda.synchronize()
         ref, bound = tolerance.reference_with_bound(g, ins)
         assert tolerance.check(d_out[0].cpu().numpy(), ref[0], bound[0])[0]
+
+
+def test_bert_bench_plan_anchored_parity():
+    """The bench's BERT plan (the shipped 12-layer plan's fusion groups) at
+    full widths and a 1024-token batch, every one of the 182 outputs --
+    forward activations through f11_ln2_y, every backward gradient and every
+    column-reduced parameter gradient -- certified against the oracle with
+    step-wise anchoring (oracle/tolerance.py anchored_reference_with_bound:
+    consumers of an output read the executor's checked value of it, so each
+    bound covers one layer instead of twelve). No element may be left
+    uncertified. The achieved margins are written to
+    gpurun_out/bert_anchored_margins.json when that directory exists."""
+    import json
+    import os
+    g = W.bert(batch=8)
+    fused = tuning.plan_like("bert", g)
+    ins = orc.random_inputs(g, seed=83)
+    ex, got = run_device(fused, ins)
+    outs = orc.graph_outputs(g)
+    assert len(outs) == len(got) == 182
+    by_id = dict(zip(outs, got))
+    ref, bound = tolerance.anchored_reference_with_bound(g, ins, by_id)
+    rows, bad = [], []
+    for oid, r, b in zip(outs, ref, bound):
+        a = by_id[oid].astype(np.float64).reshape(r.shape)
+        base = np.maximum(tolerance.RTOL * np.abs(r), tolerance.ATOL)
+        tol = base + tolerance.SAFETY * np.nan_to_num(b, nan=np.inf, posinf=np.inf)
+        uncert = int((~np.isfinite(tol)).sum())
+        ok, worst = tolerance.check(a, r, b)
+        err = np.abs(a - r)
+        rows.append({"output": oid, "elements": int(r.size), "uncertified": uncert, "worst_err_over_tol": worst,
+                     "median_tol_over_base": float(np.median(tol / base)),
+                     "max_err_over_base": float(np.max(err / base)), "median_err_over_base": float(np.median(err / base))})
+        if not ok or uncert:
+            bad.append(rows[-1])
+    if os.path.isdir("gpurun_out"):
+        with open("gpurun_out/bert_anchored_margins.json", "w") as f:
+            json.dump({"graph": "bert(batch=8), shipped bench plan groups", "kernels": len(ex.info["kernels"]),
+                       "outputs": rows}, f, indent=1)
+    assert not bad, bad[:3]
+
+
+def test_broadcast_sinking_parity():
+    """Sunk broadcasts (consumers read the source through the broadcast map)
+    give the same results as materialised ones -- bit-identical on the
+    unfused BERT-small graph -- and pass the oracle."""
+    g = W.bert(**W.SMALL["bert"])
+    ins = orc.random_inputs(g, seed=85, scale=0.5)
+    ex_on, a = run_device(g, ins, fold_constants=False)
+    ex_off, b = run_device(g, ins, fold_constants=False, sink_broadcasts=False)
+    assert ex_on.info["sunk_broadcast_kernels"] > 0
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+    assert_parity(g, g, ins, fold_constants=False)
