@@ -404,7 +404,8 @@ def main():
         t0 = time.perf_counter()
         plan, plan_kind = tuning.config_plan(name, g)
         plan_ms = (time.perf_counter() - t0) * 1e3
-        ex = rt.Executor(plan["fused"], device=local)
+        # the measured per-group codegen variants (scripts/tune_variants.py)
+        ex = rt.Executor(plan["fused"], device=local, kernel_options=tuning.kernel_variants(name))
         model = None
         if not args.no_model_plan and plan_kind.startswith("execution"):
             mplan = rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT)
