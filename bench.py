@@ -410,7 +410,10 @@ def main():
         if not args.no_model_plan and plan_kind.startswith("execution"):
             mplan = rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT)
             model = rt.Executor(mplan["fused"], device=local)
-        base = None if args.no_unfused else rt.Executor(g, device=local, chunking=False, fold_constants=False)
+        # the unfused baseline: strictly one kernel per op (no constant
+        # folding, no broadcast sinking)
+        base = None if args.no_unfused else rt.Executor(g, device=local, chunking=False, fold_constants=False,
+                                                        sink_broadcasts=False)
         ins = [torch.randn(t["dims"], device=dev, generator=gen, dtype=torch.float32) for t in ex.info["inputs"]]
         outs = [torch.empty(t["dims"], device=dev, dtype=torch.float32) for t in ex.info["outputs"]]
         by_id = dict(zip(ex.input_ids, ins))

@@ -6,6 +6,8 @@
 // subsequence match. Reductions: sum (reference) or max (extension).
 #include "codegen.hpp"
 
+#include "../host/cost.hpp"
+
 #include <algorithm>
 #include <cstring>
 #include <functional>
@@ -158,6 +160,18 @@ class Builder {
   void emit_row(Component& c, const std::string& lo, const std::string& n, const std::string& cta_rank);
   void emit_row_finalize(std::vector<Component*>& comps);
   void emit_sectioned(const std::vector<int>& members);
+  // BLOCK: heterogeneous groups over a common leading index G (paper Fig. 1:
+  // dots + reductions + elementwise over different inner index spaces), one
+  // CTA per leading index, sections separated by __syncthreads, staged values
+  // in shared memory at the planner's Alg. 4 alloc map. Returns the shared
+  // bytes, or -1 when the group does not fit the scheme.
+  int64_t plan_block(int64_t* G);
+  void emit_block(const std::vector<int>& members, int64_t G);
+  std::string emit_heavy(int m, const std::vector<std::string>& oc);  // reduce / dot value at coords (loops)
+  bool inline_heavy_ = false;  // at() may recompute reductions and dots inline (BLOCK)
+  std::map<int, std::pair<int64_t, int64_t>> block_smem_;  // value -> (byte offset, bytes) per leading index
+  std::map<int, int> block_reuse_;  // value -> value whose shared block it reuses (planner's reused_from)
+  std::string block_alloc_note_;
 
   bool reg_input(const Component& c, int v) const;
   bool tc_direct(const Component& c, int m) const;
@@ -989,6 +1003,9 @@ std::string Builder::at(int v, const std::vector<std::string>& coords) {
       for (int o : x.operands) args.push_back(at(o, coords));
     }
     expr = elem_expr(*x.node, args);
+  } else if (inline_heavy_ && x.member &&
+             (x.node->type == OpType::kReduce || x.node->type == OpType::kDot || x.node->type == OpType::kBatchedDot)) {
+    return emit_heavy(v, coords);
   } else {
     throw InternalError("stitched executor: value " + x.id + " needed inline but not materialised");
   }
@@ -2188,6 +2205,236 @@ void Builder::emit_sectioned(const std::vector<int>& members) {
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// BLOCK: block composition of heterogeneous groups (paper Fig. 1)
+// ---------------------------------------------------------------------------
+
+int64_t Builder::plan_block(int64_t* G) {
+  if (topo_members_.empty() || !opts_.allow_row) return -1;
+  const int64_t g0 = vals_[topo_members_.front()].dims.empty() ? -1 : vals_[topo_members_.front()].dims[0];
+  if (g0 < 1) return -1;
+  auto member = [&](int v) { return vals_[v].member; };
+  for (int m : topo_members_) {
+    const Val& v = vals_[m];
+    const OpNode& op = *v.node;
+    if (v.dims.empty() || v.dims[0] != g0) return -1;
+    if (op.type == OpType::kElementwise) {
+      if (op.elem_name == "broadcast") {
+        const int in = v.operands[0];
+        if (vals_[in].constant || vals_[in].dims.empty()) continue;
+        std::vector<int> mp = broadcast_dim_map(vals_[in].node->shape, op.shape);
+        const bool batched = vals_[in].dims[0] == g0 && !mp.empty() && mp[0] == 0;
+        if (member(in) && !batched) return -1;  // a computed value's leading index moves
+      } else {
+        for (int o : v.operands)
+          if (!vals_[o].constant && vals_[o].dims != v.dims && member(o)) return -1;
+      }
+    } else if (op.type == OpType::kReduce) {
+      if (std::find(op.reduce_dims.begin(), op.reduce_dims.end(), 0) != op.reduce_dims.end()) return -1;
+    } else if (op.type == OpType::kBatchedDot) {
+      if (v.dims.size() < 3) return -1;
+    } else if (op.type == OpType::kDot) {
+      auto cd = effective_contract_dims(body_, op);
+      if (cd[0] == 0 || member(v.operands[1])) return -1;
+    } else {
+      return -1;
+    }
+  }
+  // Shared memory: the planner's Alg. 4 alloc map for this group (requests
+  // and post-dominance reuse, cost.cpp shared_planning), per leading index.
+  FusionPattern pat;
+  for (int m : topo_members_) pat.node_ids.insert(vals_[m].id);
+  AllocMap am = shared_planning(body_, pat, canonical_shared_requests(body_, pat));
+  std::map<std::string, int> idx;
+  for (int m : topo_members_) idx[vals_[m].id] = m;
+  int64_t total = 0;
+  block_smem_.clear();
+  block_reuse_.clear();
+  for (const AllocEntry& e : am.entries) {
+    auto it = idx.find(e.op_id);
+    if (it == idx.end()) continue;  // "<op>__tree" scratch: reductions here run per element
+    const int m = it->second;
+    const int64_t bytes = (prod(vals_[m].dims, 1) * 4 + 15) / 16 * 16;
+    if (e.reused_from && idx.count(*e.reused_from) && block_smem_.count(idx[*e.reused_from]) &&
+        block_smem_[idx[*e.reused_from]].second >= bytes) {
+      block_smem_[m] = {block_smem_[idx[*e.reused_from]].first, bytes};
+      block_reuse_[m] = idx[*e.reused_from];
+    } else {
+      block_smem_[m] = {total, bytes};
+      total += bytes;
+    }
+  }
+  if (total > opts_.max_smem) return -1;
+  std::ostringstream note;
+  note << "planner alloc total " << am.total << " B, requested " << am.requested() << " B";
+  block_alloc_note_ = note.str();
+  *G = g0;
+  return total;
+}
+
+
+std::string Builder::emit_heavy(int m, const std::vector<std::string>& oc) {
+  const Val& v = vals_[m];
+  const OpNode& op = *v.node;
+  const std::string acc = fresh("acc");
+  if (op.type == OpType::kReduce) {
+    const int in = v.operands[0];
+    const auto& ind = vals_[in].dims;
+    const std::string Op = op.elem_name == "max" ? "stitch_dev::MaxOp" : "stitch_dev::SumOp";
+    ln("float " + acc + " = " + Op + "::init();  // " + v.id);
+    std::vector<std::string> ic;
+    size_t kept = 0;
+    int loops = 0;
+    for (size_t d = 0; d < ind.size(); ++d) {
+      if (std::find(op.reduce_dims.begin(), op.reduce_dims.end(), static_cast<int>(d)) != op.reduce_dims.end()) {
+        std::string lv = fresh("q");
+        open("for (long long " + lv + " = 0; " + lv + " < " + std::to_string(ind[d]) + "LL; ++" + lv + ")");
+        memo_.emplace_back();
+        ++loops;
+        ic.push_back(lv);
+      } else {
+        ic.push_back(oc[kept++]);
+      }
+    }
+    ln(acc + " = " + Op + "::apply(" + acc + ", " + at(in, ic) + ");");
+    for (int l = 0; l < loops; ++l) {
+      memo_.pop_back();
+      close();
+    }
+    return acc;
+  }
+  const int a = v.operands[0], b = v.operands[1];
+  auto cd = effective_contract_dims(body_, op);
+  const int64_t K = vals_[a].dims[cd[0]];
+  std::vector<std::string> ac, bc;
+  const std::string kk = fresh("k");
+  if (op.type == OpType::kBatchedDot) {
+    const int r = static_cast<int>(v.dims.size());
+    for (int d = 0; d < r - 2; ++d) {
+      ac.push_back(oc[d]);
+      bc.push_back(oc[d]);
+    }
+    ac.push_back(oc[r - 2]);
+    ac.push_back(kk);
+    bc.push_back(kk);
+    bc.push_back(oc[r - 1]);
+  } else {
+    int pos = 0;
+    for (int d = 0; d < static_cast<int>(vals_[a].dims.size()); ++d) ac.push_back(d == cd[0] ? kk : oc[pos++]);
+    for (int d = 0; d < static_cast<int>(vals_[b].dims.size()); ++d) bc.push_back(d == cd[1] ? kk : oc[pos++]);
+  }
+  ln("float " + acc + " = 0.f;  // " + v.id);
+  open("for (long long " + kk + " = 0; " + kk + " < " + std::to_string(K) + "LL; ++" + kk + ")");
+  memo_.emplace_back();
+  ln(acc + " = fmaf(" + at(a, ac) + ", " + at(b, bc) + ", " + acc + ");");
+  memo_.pop_back();
+  close();
+  return acc;
+}
+
+void Builder::emit_block(const std::vector<int>& members, int64_t G) {
+  // materialised values: outputs, reductions, dots, dot operands, and the
+  // planner's shared-memory values; everything else is recomputed inline
+  // (a reduction or dot with a single elementwise consumer over its own index
+  // space is computed inline in that consumer's section, as the reference's
+  // sketches do -- e.g. fig1's dot_2 inside divide)
+  std::vector<int> mat;
+  for (int m : members) {
+    const Val& v = vals_[m];
+    bool need = v.output || block_smem_.count(m);
+    if (v.node->type != OpType::kElementwise) {
+      int in_group = 0;
+      bool simple = true;
+      for (int c : v.consumers) {
+        if (!vals_[c].member) continue;
+        ++in_group;
+        simple = simple && vals_[c].node->type == OpType::kElementwise && vals_[c].node->elem_name != "broadcast" &&
+                 vals_[c].dims == v.dims;
+      }
+      need = need || in_group != 1 || !simple;
+    }
+    for (int c : v.consumers)
+      need = need || vals_[c].node->type == OpType::kDot || vals_[c].node->type == OpType::kBatchedDot;
+    if (need) mat.push_back(m);
+  }
+  inline_heavy_ = true;
+  // per-CTA workspace for materialised values neither in shared memory nor outputs
+  int64_t wsb = 0;
+  std::map<int, int64_t> wso;
+  for (int m : mat)
+    if (!vals_[m].output && !block_smem_.count(m)) {
+      wso[m] = wsb;
+      wsb += (prod(vals_[m].dims, 1) + 63) / 64 * 64;
+    }
+  const int64_t ws_base = ws_floats_;
+  ws_floats_ += wsb * static_cast<int64_t>(opts_.num_sms) * 8;  // one slice per resident CTA (grid <= 8 x SMs)
+  ln("// block composition: one CTA per leading index g < " + std::to_string(G) + "; " + block_alloc_note_);
+  for (auto& [m, ob] : block_smem_)
+    ln("float* sh" + std::to_string(m) + " = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(smem) + " +
+       std::to_string(ob.first) + ");  // " + vals_[m].id + (block_reuse_.count(m) ? " (reuses " + vals_[block_reuse_[m]].id + ")" : ""));
+  ln("float* wsb = ws + " + std::to_string(ws_base) + "LL + (long long)blockIdx.x * " + std::to_string(wsb) + "LL;");
+  ln("(void)wsb;");
+  std::set<int> done;
+  row_hook_ = [&](int v, const std::vector<std::string>& coords) -> std::string {
+    if (!done.count(v)) return "";
+    std::vector<std::string> inner(coords.begin() + 1, coords.end());
+    std::vector<int64_t> idims(vals_[v].dims.begin() + 1, vals_[v].dims.end());
+    const std::string lin = idims.empty() ? std::string("0") : linear(inner, idims);
+    if (block_smem_.count(v)) return "sh" + std::to_string(v) + "[" + lin + "]";
+    if (wso.count(v)) return "wsb[" + std::to_string(wso[v]) + "LL + " + lin + "]";
+    return "__ldcg(" + out_ptr(v) + " + " + linear(coords, vals_[v].dims) + ")";
+  };
+  open("for (long long g = blockIdx.x; g < " + std::to_string(G) + "LL; g += gridDim.x)");
+  for (size_t s = 0; s < mat.size(); ++s) {
+    const int m = mat[s];
+    const Val& v = vals_[m];
+    const OpNode& op = *v.node;
+    const int64_t inner = prod(v.dims, 1);
+    std::vector<int64_t> idims(v.dims.begin() + 1, v.dims.end());
+    // A value that reuses another's shared block is computed into registers
+    // first, then written after a barrier (its section may still read the
+    // block it overwrites); one register slot per element of the thread.
+    const bool two_phase = block_reuse_.count(m) > 0;
+    const int64_t per_thread = (inner + 255) / 256;
+    ln("// section " + std::to_string(s) + ": " + v.id + (block_smem_.count(m) ? " -> shared" : v.output ? " -> output" : " -> workspace"));
+    if (two_phase) ln("float st" + std::to_string(m) + "[" + std::to_string(per_thread) + "];");
+    open("for (long long i = threadIdx.x, slot = 0; i < " + std::to_string(inner) + "LL; i += blockDim.x, ++slot)");
+    ln("(void)slot;");
+    memo_.emplace_back();
+    std::vector<std::string> oc = {"g"};
+    for (const std::string& c : decode("i", idims)) oc.push_back(c);
+    if (idims.empty()) oc.resize(1);
+    std::string val;
+    if (op.type == OpType::kElementwise) {
+      val = at(m, oc);
+    } else {
+      val = emit_heavy(m, oc);
+    }
+    if (two_phase) {
+      ln("st" + std::to_string(m) + "[slot] = " + val + ";");
+    } else {
+      if (block_smem_.count(m)) ln("sh" + std::to_string(m) + "[i] = " + val + ";");
+      else if (wso.count(m)) ln("wsb[" + std::to_string(wso[m]) + "LL + i] = " + val + ";");
+      if (v.output) ln(out_ptr(m) + "[g * " + std::to_string(inner) + "LL + i] = " + val + ";");
+    }
+    memo_.pop_back();
+    close();
+    if (two_phase) {
+      ln("__syncthreads();  // every reader of the block " + vals_[m].id + " reuses is done");
+      open("for (long long i = threadIdx.x, slot = 0; i < " + std::to_string(inner) + "LL; i += blockDim.x, ++slot)");
+      ln("sh" + std::to_string(m) + "[i] = st" + std::to_string(m) + "[slot];");
+      if (v.output) ln(out_ptr(m) + "[g * " + std::to_string(inner) + "LL + i] = st" + std::to_string(m) + "[slot];");
+      close();
+    }
+    ln("__syncthreads();");
+    done.insert(m);
+  }
+  close();
+  row_hook_ = nullptr;
+  inline_heavy_ = false;
+}
+
 // ---------------------------------------------------------------------------
 // driver
 // ---------------------------------------------------------------------------
@@ -2435,7 +2682,20 @@ KernelSpec Builder::build() {
   std::ostringstream head;
   std::string body_src;
   int64_t smem_floats = 0;
-  if (sectioned) {
+  int64_t block_G = 0, block_smem = -1;
+  if (sectioned && opts_.block_compose) block_smem = plan_block(&block_G);
+  if (sectioned && block_smem >= 0) {
+    spec_.scheme = "block(G=" + std::to_string(block_G) + ",smem=" + std::to_string(block_smem) + ")";
+    spec_.composition = {"thread", "block"};
+    memo_.emplace_back();
+    indent_ = 1;
+    emit_block(topo_members_, block_G);
+    memo_.pop_back();
+    body_src = out_.str();
+    block = 256;
+    spec_.max_grid = static_cast<int>(std::min<int64_t>(block_G, static_cast<int64_t>(opts_.num_sms) * 8));
+    smem_floats = (block_smem + 3) / 4;
+  } else if (sectioned) {
     spec_.scheme = "sectioned";
     spec_.cooperative = true;
     spec_.composition = {"block"};

@@ -88,6 +88,11 @@ struct CodegenOptions {
   // (the GRU group): the warp-specialised tcgen05 scheme (device gws::run,
   // TMA producer / MMA issuer / split / tail warps). Off: the ROW scheme.
   bool gws = true;
+  // Groups ROW / COLRED / FLAT cannot take (dots + reductions over different
+  // index spaces, paper Fig. 1) run as BLOCK composition -- one CTA per
+  // leading index, shared memory at the planner's Alg. 4 alloc map -- instead
+  // of grid-barrier SECTIONED when they share a leading index.
+  bool block_compose = true;
   bool tma_early = false;  // CTA rows: next row's TMA tiles requested as soon as their last reader is done
   bool cross_smem = true;  // warp rows: many column-reduction partials in the warp's shared slab
   int cross_smem_min_regs = 16;  // ... when they would take more than this many registers per lane

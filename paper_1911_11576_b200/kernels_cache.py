@@ -88,7 +88,7 @@ def prebuild(verbose=True, workers=None):
     import os
     jobs = []
     for tag, fused in plans():
-        opts = {"chunking": False, "fold_constants": False} if tag.endswith("/unfused") else {}
+        opts = {"chunking": False, "fold_constants": False, "sink_broadcasts": False} if tag.endswith("/unfused") else {}
         if tag.endswith("/bench"):
             opts["kernel_options"] = tuning.kernel_variants(tag.split("/")[0])
         jobs.append((json.dumps(fused), opts))

@@ -24,7 +24,7 @@ for name in a.configs.split(","):
     if a.unfused:
         graphs.append(("unfused", g))
     for tag, fg in graphs:
-        ex = rt.Executor(fg, use_graph=False, **({} if tag == "fused" else {"fold_constants": False}))
+        ex = rt.Executor(fg, use_graph=False, **({"kernel_options": tuning.kernel_variants(name)} if tag == "fused" else {"fold_constants": False, "sink_broadcasts": False}))
         ins = [torch.randn(t["dims"], device="cuda") for t in ex.info["inputs"]]
         outs = [torch.empty(t["dims"], device="cuda") for t in ex.info["outputs"]]
         for _ in range(a.iters):

@@ -26,8 +26,10 @@ def test_b200_plans_compile(name, size):
     groups = sum(1 for n in fused["nodes"] if n["kind"] == "fused")
     unfused = sum(1 for n in fused["nodes"] if n["kind"] in ("elementwise", "reduce", "dot", "batched_dot"))
     # one kernel per fusion group / kernel op, except unfused broadcasts of
-    # constants, which are folded into their consumers as literals
-    assert len(ex.info["kernels"]) + ex.info["folded_constant_kernels"] == groups + unfused
+    # constants (folded into their consumers as literals) and of small
+    # tensors (sunk into their consumers' bodies)
+    assert (len(ex.info["kernels"]) + ex.info["folded_constant_kernels"] + ex.info["sunk_broadcast_kernels"]
+            == groups + unfused)
     for k in ex.info["kernels"]:
         assert k["block"] % 32 == 0 and k["smem_bytes"] <= 232448
 
@@ -77,7 +79,7 @@ def test_sectioned_fallback_compiles(name):
 
 def test_unfused_baseline_one_kernel_per_op():
     g = W.softmax(**W.SMALL["softmax"])
-    ex = compile_only(g, fold_constants=False)  # the bench's unfused baseline
+    ex = compile_only(g, fold_constants=False, sink_broadcasts=False)  # the bench's unfused baseline
     ops = [n for n in g["nodes"] if n["kind"] in ("elementwise", "reduce", "dot", "batched_dot")]
     assert len(ex.info["kernels"]) == len(ops)
 
@@ -132,3 +134,34 @@ def test_broadcast_sinking():
     g["nodes"][-1]["operands"] = ["y", "z", "gb"]
     info = compile_only(g).info
     assert info["sunk_broadcast_kernels"] == 0 and len(info["kernels"]) == 3
+
+
+def test_fig1_block_composition():
+    """Paper Fig. 1 (the reference's fig1 fixture, one fused group of two
+    batched dots, two reductions over different index spaces and elementwise
+    ops) runs as BLOCK composition: one CTA per leading index, no grid
+    barrier, shared memory exactly the planner's Alg. 4 alloc map (dot_1's
+    35,344-byte block reused by add: alloc / requested = 0.5), the second dot
+    computed inside its consumer's section."""
+    import json
+    import os
+    fx = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "ref_sketches.json")
+    g = next(e for e in json.load(open(fx)) if e["name"] == "fixture:fig1")["graph"]
+    for lim in (W.REFERENCE_SHARED_LIMIT, W.B200_SHARED_LIMIT):
+        fused = rt.plan(g, shared_limit_bytes=lim)["fused"]
+        info = rt.debug_call("pattern_info", graph=g, nodes=[n["id"] for n in g["nodes"] if n["kind"] not in ("parameter", "tuple")])
+        assert info["alloc"]["total"] == 35344 and info["requested"] == 2 * 35344
+        (k,) = compile_only(fused).info["kernels"]
+        assert k["scheme"] == "block(G=1,smem=35344)" and not k["cooperative"]
+        assert k["smem_bytes"] - 16 == info["alloc"]["total"]
+        assert "block" in k["composition"]
+
+
+def test_block_scheme_off_falls_back_to_sectioned():
+    import json
+    import os
+    fx = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "ref_sketches.json")
+    g = next(e for e in json.load(open(fx)) if e["name"] == "fixture:fig1")["graph"]
+    fused = rt.plan(g)["fused"]
+    (k,) = compile_only(fused, block_compose=False).info["kernels"]
+    assert k["scheme"] == "sectioned" and k["cooperative"]
