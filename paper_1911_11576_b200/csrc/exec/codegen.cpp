@@ -106,6 +106,7 @@ struct Component {
   // COLRED: a lone column reduction of an external [R][C] tensor
   int64_t cr_R = 0, cr_C = 0, cr_ncb = 0, cr_nch = 0, cr_rpc = 0;
   int cr_sync = 0, cr_m = -1, cr_w = 128;
+  int cr_cluster = 0;         // COLRED: row chunks of a column block form a cluster of this many CTAs
   bool tc = false;            // gemm stages on tcgen05 (3xTF32): smem scratch + TMEM accumulator
   int tc_k = 0;               // largest K among the tensor-core gemm stages
   std::vector<char> tc_dot;   // value -> gemm stage runs on tcgen05
@@ -391,6 +392,14 @@ bool Builder::plan_colred(Component& c) {
   // at least one full pass of the CTA's row groups per chunk
   const int64_t pass = 8 * (128 / W);
   nch = std::min<int64_t>(nch, std::max<int64_t>(1, c.cr_R / pass));
+  // cluster combine: exactly colred_cluster chunks per column block (one
+  // cluster each), when every chunk keeps at least one full pass
+  const int K = opts_.colred_cluster;
+  c.cr_cluster = 0;
+  if ((K == 2 || K == 4 || K == 8 || K == 16) && c.cr_R >= static_cast<int64_t>(K) * pass) {
+    c.cr_cluster = K;
+    nch = K;
+  }
   // chunks of whole passes: every pass but the matrix's last is unpredicated
   c.cr_rpc = ((c.cr_R + nch - 1) / nch + pass - 1) / pass * pass;
   c.cr_nch = (c.cr_R + c.cr_rpc - 1) / c.cr_rpc;
@@ -419,7 +428,10 @@ void Builder::emit_colred(Component& c, const std::string& lo, const std::string
   ln("const int sub = lane / " + std::to_string(LPR) + ", cl = lane % " + std::to_string(LPR) + ";");
   ln("int* last = reinterpret_cast<int*>(smem + " + std::to_string(kColredStageOff - 8) + ");  // past every partial row");
   open("for (long long tile = (long long)blockIdx.x - " + lo + "; tile < " + NCB + "LL * " + NCH + "LL; tile += " + n + ")");
-  ln("const int cb = (int)(tile % " + NCB + "), ch = (int)(tile / " + NCB + ");");
+  if (c.cr_cluster)  // the K row chunks of a column block are one cluster (consecutive CTAs)
+    ln("const int cb = (int)(tile / " + std::to_string(c.cr_cluster) + "), ch = (int)(tile % " + std::to_string(c.cr_cluster) + ");");
+  else
+    ln("const int cb = (int)(tile % " + NCB + "), ch = (int)(tile / " + NCB + ");");
   ln("const long long col = (long long)cb * " + Ws + " + cl * 4;");
   ln("const long long r0 = (long long)ch * " + std::to_string(c.cr_rpc) + "LL;");
   ln("const long long r1 = r0 + " + std::to_string(c.cr_rpc) + "LL < " + std::to_string(c.cr_R) + "LL ? r0 + " +
@@ -521,6 +533,31 @@ void Builder::emit_colred(Component& c, const std::string& lo, const std::string
   open("if ((long long)cb * " + Ws + " + i < " + C + ")");
   ln("float a = " + Op + "::init();");
   ln("for (int w = 0; w < nw; ++w) a = " + Op + "::apply(a, smem[w * " + Ws + " + i]);");
+  if (c.cr_cluster) {
+    // this chunk's partial row stays in shared memory (the staging area,
+    // free now); rank 0 folds the cluster's K partials in rank order
+    // through DSMEM after a cluster barrier
+    const std::string K = std::to_string(c.cr_cluster);
+    ln("smem[" + std::to_string(kColredStageOff) + " + i] = a;");
+    close();
+    close();
+    ln("stitch_dev::cluster_sync();");
+    open("if (ch == 0)");
+    open("for (int i = threadIdx.x; i < " + Ws + "; i += blockDim.x)");
+    open("if ((long long)cb * " + Ws + " + i < " + C + ")");
+    ln("float v = " + Op + "::init();");
+    ln("#pragma unroll");
+    ln("for (unsigned r = 0; r < " + K + "u; ++r) v = " + Op + "::apply(v, stitch_dev::dsmem_ld(smem + " +
+       std::to_string(kColredStageOff) + " + i, r));");
+    ln(out_ptr(m) + "[(long long)cb * " + Ws + " + i] = v;");
+    close();
+    close();
+    close();
+    ln("stitch_dev::cluster_sync();  // every remote read of this CTA's partial is done");
+    close();
+    close();
+    return;
+  }
   ln(parts + "[(long long)ch * " + C + " + (long long)cb * " + Ws + " + i] = a;");
   close();
   close();
@@ -2824,7 +2861,8 @@ KernelSpec Builder::build() {
         spec_.composition.insert("block");
         smem_floats = std::max<int64_t>(smem_floats, opts_.colred_cp_async ? kColredStageOff + 256 * 4 * kColredStageSlots : kColredStageOff);
         std::ostringstream cs;
-        cs << "colred(" << c.cr_ncb << "x" << c.cr_nch << ",w" << c.cr_w << ")";
+        cs << "colred(" << c.cr_ncb << "x" << c.cr_nch << ",w" << c.cr_w << (c.cr_cluster ? ",cluster" : "") << ")";
+        if (c.cr_cluster) spec_.cluster = c.cr_cluster;
         scheme += (scheme.empty() ? "" : "+") + cs.str();
         spec_.max_grid = std::max<int>(spec_.max_grid, static_cast<int>(std::min<int64_t>(c.max_grid, 1 << 20)));
       } else {

@@ -53,6 +53,7 @@ struct KernelSpec {
   // them with any warp count <= block; shared memory scales per warp.
   bool flex_block = false;
   int min_grid = 1;                  // ranged packing: at least one CTA per component
+  int cluster = 0;                   // thread-block cluster size (1-D); grid = max_grid exactly
   // TMA tensor maps passed by value after the standard arguments (gws scheme):
   // input argument index, box rows, 0 = 128B swizzle (K-major A operand),
   // 1 = 128B swizzle of 32-byte atoms (MN-major B operand); [S][64][64] fp32
@@ -97,6 +98,11 @@ struct CodegenOptions {
   bool cross_smem = true;  // warp rows: many column-reduction partials in the warp's shared slab
   int cross_smem_min_regs = 16;  // ... when they would take more than this many registers per lane
   int colred_ctas_per_sm = 4;  // COLRED tiles per SM (one resident wave)
+  // COLRED row chunks of a column block as one thread-block cluster of this
+  // many CTAs, combined through distributed shared memory (cluster barrier
+  // + DSMEM loads, fixed rank order) instead of global partials + fence +
+  // arrival counter + last-CTA fold; 0: the global scheme
+  int colred_cluster = 16;  // BERT step 2.257 -> 2.195 ms (8: 2.205; 2: 2.473)
   int colred_cols = 32;        // COLRED column-block width: 32, 64 or 128 floats (32: BERT 2387 -> 2375 us)
   bool colred_cp_async = true;  // COLRED loads staged through cp.async (all of a pass in flight)  // COLRED also for reduces of an inline elementwise producer chain
   // many-input rows: load inputs per fused-loop step, not per row (measured

@@ -121,6 +121,7 @@ void apply_codegen_options(CodegenOptions& c, const json::Value& o) {
   if (o.has("colred_cp_async")) c.colred_cp_async = o.at("colred_cp_async").as_bool();
   if (o.has("colred_cols")) c.colred_cols = static_cast<int>(o.at("colred_cols").as_int());
   if (o.has("colred_ctas_per_sm")) c.colred_ctas_per_sm = static_cast<int>(o.at("colred_ctas_per_sm").as_int());
+  if (o.has("colred_cluster")) c.colred_cluster = static_cast<int>(o.at("colred_cluster").as_int());
   if (o.has("loop_fusion")) c.loop_fusion = o.at("loop_fusion").as_bool();
   if (o.has("row_prefetch")) c.row_prefetch = o.at("row_prefetch").as_bool();
   if (o.has("tma_double_buffer")) c.tma_double_buffer = o.at("tma_double_buffer").as_bool();
@@ -565,6 +566,14 @@ void Executor::init_device() {
       throw std::runtime_error("kernel " + k.spec.name + ": packed components need " + std::to_string(k.spec.min_grid) +
                                " resident CTAs");
     if (k.spec.cooperative) k.grid = static_cast<int>(std::min<int64_t>(k.grid, static_cast<int64_t>(sms_) * 32));
+    if (k.spec.cluster > 0) {
+      // cluster kernels map CTAs to work statically: exactly max_grid CTAs
+      // (a multiple of the cluster size), clusters scheduled in waves
+      k.grid = k.spec.max_grid;
+      if (k.grid % k.spec.cluster != 0) throw InternalError("cluster kernel grid is not a multiple of its cluster");
+      if (k.spec.cluster > 8)
+        cu_check(cu.cuFuncSetAttribute(fn, CU_FUNC_ATTRIBUTE_NON_PORTABLE_CLUSTER_SIZE_ALLOWED, 1), "cluster attribute");
+    }
   }
   cubins_tmp_.clear();
   int lanes = 0, nev = 0;
@@ -655,19 +664,26 @@ void Executor::launch_one(int i, int c, int chunks, const void* const* inputs, v
   cfg.blockDimY = cfg.blockDimZ = 1;
   cfg.sharedMemBytes = k.smem;
   cfg.hStream = static_cast<CUstream>(stream);
-  CUlaunchAttribute attr[1];
+  CUlaunchAttribute attr[2];
+  unsigned na_attr = 0;
   if (k.spec.cooperative) {
-    attr[0].id = CU_LAUNCH_ATTRIBUTE_COOPERATIVE;
-    attr[0].value.cooperative = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    attr[na_attr].id = CU_LAUNCH_ATTRIBUTE_COOPERATIVE;
+    attr[na_attr++].value.cooperative = 1;
   } else if (opts_.pdl) {
     // overlap this launch with the previous kernel's tail (the kernel waits
     // in griddepcontrol.wait before reading anything)
-    attr[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
-    attr[0].value.programmaticStreamSerializationAllowed = 1;
+    attr[na_attr].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+    attr[na_attr++].value.programmaticStreamSerializationAllowed = 1;
+  }
+  if (k.spec.cluster > 0) {
+    attr[na_attr].id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
+    attr[na_attr].value.clusterDim.x = static_cast<unsigned>(k.spec.cluster);
+    attr[na_attr].value.clusterDim.y = 1;
+    attr[na_attr++].value.clusterDim.z = 1;
+  }
+  if (na_attr) {
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = na_attr;
   }
   cu_check(cu.cuLaunchKernelEx(&cfg, static_cast<CUfunction>(k.fn), args.data(), nullptr), k.spec.name.c_str());
 }

@@ -38,6 +38,8 @@ VARIANTS = [
     {"loop_fusion": False},
     {"colred_cols": 64},
     {"colred_cols": 128},
+    {"colred_cluster": 8},
+    {"colred_cluster": 0},
     {"pack_sequential": True},
     {"tma_double_buffer": True},
 ]
@@ -102,23 +104,25 @@ def main():
                                                                         else t_def, 2),
                       "variant": VARIANTS[best_v] if op in table else {}}
 
-    def step_ms(ex):
-        ts = []
-        for _ in range(10):
-            flush_l2()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(s)
-            ex.run(ins, outs, stream=s.cuda_stream)
-            e1.record(s)
-            torch.cuda.synchronize()
-            ts.append(e0.elapsed_time(e1))
-        return float(np.median(ts))
+    def step_once(ex):
+        flush_l2()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        ex.run(ins, outs, stream=s.cuda_stream)
+        e1.record(s)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1)
 
     ex0 = rt.Executor(fused)
     ex1 = rt.Executor(fused, kernel_options=table)
-    step0, step1 = step_ms(ex0), step_ms(ex1)
+    t0s, t1s = [], []
+    for i in range(30):  # alternating, so clock / thermal drift hits both
+        t0s.append(step_once(ex0))
+        t1s.append(step_once(ex1))
+    step0, step1 = float(np.median(t0s[5:])), float(np.median(t1s[5:]))
     print("step: default %.4f ms, tuned %.4f ms (%d of %d groups changed)" % (step0, step1, len(table), len(base)))
-    res = {"config": a.config, "variants": VARIANTS, "table": table, "per_op": chosen,
+    all_times = {op: {str(vi): round(tv[op], 2) for vi, tv in times.items() if op in tv} for op in base}
+    res = {"config": a.config, "variants": VARIANTS, "table": table, "per_op": chosen, "times_us": all_times,
            "step_ms": {"default": step0, "tuned": step1}, "reps": a.reps, "min_gain": a.min_gain}
     out = a.out or os.path.join(ROOT, "paper_1911_11576_b200", "data", "kernel_variants", a.config + ".json")
     os.makedirs(os.path.dirname(out), exist_ok=True)
