@@ -403,6 +403,9 @@ bool Builder::plan_colred(Component& c) {
   // chunks of whole passes: every pass but the matrix's last is unpredicated
   c.cr_rpc = ((c.cr_R + nch - 1) / nch + pass - 1) / pass * pass;
   c.cr_nch = (c.cr_R + c.cr_rpc - 1) / c.cr_rpc;
+  // a cluster always has K chunks (trailing ones may be empty: their
+  // partial is the reduction's identity)
+  if (c.cr_cluster) c.cr_nch = c.cr_cluster;
   c.cr_sync = colred_sync_;
   colred_sync_ += static_cast<int>(c.cr_ncb);
   c.scheme = "colred";
@@ -2860,6 +2863,7 @@ KernelSpec Builder::build() {
         emit_colred(c, lo[i], n[i]);
         spec_.composition.insert("block");
         smem_floats = std::max<int64_t>(smem_floats, opts_.colred_cp_async ? kColredStageOff + 256 * 4 * kColredStageSlots : kColredStageOff);
+        if (c.cr_cluster) smem_floats = std::max<int64_t>(smem_floats, kColredStageOff + c.cr_w);  // the cluster partial row
         std::ostringstream cs;
         cs << "colred(" << c.cr_ncb << "x" << c.cr_nch << ",w" << c.cr_w << (c.cr_cluster ? ",cluster" : "") << ")";
         if (c.cr_cluster) spec_.cluster = c.cr_cluster;
@@ -2935,6 +2939,8 @@ KernelSpec Builder::build() {
   spec_.sync_words = std::max((spec_.cooperative || uses_barrier_) ? 2 : 0, colred_sync_ > 2 ? colred_sync_ : 0);
   if (uses_barrier_) spec_.cooperative = true;
   if (spec_.max_grid < 1) spec_.max_grid = 1;
+  if (spec_.cluster > 0 && spec_.max_grid % spec_.cluster != 0)
+    throw InternalError("stitched executor: cluster kernel " + name_ + " grid is not a multiple of its cluster");
   return spec_;
 }
 

@@ -165,3 +165,20 @@ def test_block_scheme_off_falls_back_to_sectioned():
     fused = rt.plan(g)["fused"]
     (k,) = compile_only(fused, block_compose=False).info["kernels"]
     assert k["scheme"] == "sectioned" and k["cooperative"]
+
+
+@pytest.mark.parametrize("seed", range(0, 64, 3))
+def test_random_dag_kernels_compile(seed):
+    """Every kernel of seeded random DAGs compiles under the default and the
+    non-default codegen paths (cluster COLRED grids a multiple of the
+    cluster, BLOCK / ROW / COLRED / FLAT)."""
+    from helpers import random_dag
+    R = [3, 64, 100, 257, 1024, 1, 2, 4096][seed % 8]
+    C = [4, 33, 256, 768, 1000, 1, 2, 2048][(seed // 8) % 8]
+    g = random_dag(seed, n_ops=6 + seed % 10, dims=(R, C))
+    fused = rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT)["fused"]
+    for opts in ({}, dict(row_prefetch_warp=True, colred_cols=128, tma_early=True, cross_smem=False,
+                          colred_cp_async=False), dict(colred_cluster=8), dict(colred_cluster=0)):
+        for gg in (fused, g):
+            for k in compile_only(gg, **opts).info["kernels"]:
+                assert k["block"] % 32 == 0
