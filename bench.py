@@ -414,6 +414,9 @@ def main():
         # folding, no broadcast sinking)
         base = None if args.no_unfused else rt.Executor(g, device=local, chunking=False, fold_constants=False,
                                                         sink_broadcasts=False)
+        # context for the geomean (not the baseline): the unfused graph with
+        # constants folded and small broadcasts sunk into their consumers
+        basef = None if args.no_unfused else rt.Executor(g, device=local, chunking=False)
         ins = [torch.randn(t["dims"], device=dev, generator=gen, dtype=torch.float32) for t in ex.info["inputs"]]
         outs = [torch.empty(t["dims"], device=dev, dtype=torch.float32) for t in ex.info["outputs"]]
         by_id = dict(zip(ex.input_ids, ins))
@@ -421,7 +424,15 @@ def main():
         outs_b = [torch.empty(t["dims"], device=dev, dtype=torch.float32) for t in base.info["outputs"]] if base else None
         ins_m = [by_id[i] for i in model.input_ids] if model else None
         outs_m = [torch.empty(t["dims"], device=dev, dtype=torch.float32) for t in model.info["outputs"]] if model else None
+        ins_f = [by_id[i] for i in basef.input_ids] if basef else None
+        outs_f = [torch.empty(t["dims"], device=dev, dtype=torch.float32) for t in basef.info["outputs"]] if basef else None
+        # same-size copy: a device copy moving the config's algorithmic bytes
+        # (half read, half written) -- the practical ceiling beside the peak
+        ncp = max(1, graph_bytes(g) // 8)
+        cp_src = torch.empty(ncp, device=dev, dtype=torch.float32)
+        cp_dst = torch.empty(ncp, device=dev, dtype=torch.float32)
         cfgs.append(dict(name=name, g=g, ex=ex, base=base, ins=ins, outs=outs, ins_b=ins_b, outs_b=outs_b,
+                         basef=basef, ins_f=ins_f, outs_f=outs_f, cp_src=cp_src, cp_dst=cp_dst,
                          model=model, ins_m=ins_m, outs_m=outs_m, plan_kind=plan_kind,
                          bytes=graph_bytes(g), plan_ms=plan_ms,
                          groups=sum(1 for n in plan["fused"]["nodes"] if n["kind"] == "fused"),
@@ -447,6 +458,10 @@ def main():
                 elif which == "model":
                     if c["model"]:
                         c["model"].run(c["ins_m"], c["outs_m"], stream=sh)
+                elif which == "unfused_folded":
+                    c["basef"].run(c["ins_f"], c["outs_f"], stream=sh)
+                elif which == "copy":
+                    c["cp_dst"].copy_(c["cp_src"])
                 else:
                     c["base"].run(c["ins_b"], c["outs_b"], stream=sh)
                 ev_pairs[i][1].record(stream)
@@ -486,9 +501,11 @@ def main():
 
     clocks = Clocks(local)
     fused_ms, ck = measure("fused", args.steps, max(3, args.warmup), clocks)
-    base_ms = None
+    base_ms = basef_ms = None
     if not args.no_unfused:
         base_ms, _ = measure("unfused", args.steps, max(3, args.warmup))
+        basef_ms, _ = measure("unfused_folded", args.steps, max(3, args.warmup))
+    copy_ms, _ = measure("copy", args.steps, max(3, args.warmup))
     model_ms = None
     if any(c["model"] for c in cfgs):
         model_ms, _ = measure("model", args.steps, max(3, args.warmup))
@@ -524,10 +541,15 @@ def main():
              "plan_ms": round(c["plan_ms"], 1),
              "kernel_us": {k: round(v[0], 2) for k, v in kstats[c["name"]].items()},
              "kernel_frac_of_hbm": {k: round(v[1] / (v[0] * 1e-6) / 1e9 / peak, 3) for k, v in kstats[c["name"]].items()}}
+        e["same_size_copy_GBps"] = round(c["bytes"] / (copy_ms[i] * 1e-3) / 1e9, 1)
+        e["frac_of_same_size_copy"] = round(float(copy_ms[i] / fused_ms[i]), 3)
         if base_ms is not None:
             sp = float(base_ms[i] / fused_ms[i])
             e.update({"unfused_GBps": round(c["bytes"] / (base_ms[i] * 1e-3) / 1e9, 1),
-                      "unfused_kernels": len(c["base"].info["kernels"]), "speedup_vs_unfused": round(sp, 3)})
+                      "unfused_kernels": len(c["base"].info["kernels"]), "speedup_vs_unfused": round(sp, 3),
+                      "unfused_folded_GBps": round(c["bytes"] / (basef_ms[i] * 1e-3) / 1e9, 1),
+                      "unfused_folded_kernels": len(c["basef"].info["kernels"]),
+                      "speedup_vs_unfused_folded": round(float(basef_ms[i] / fused_ms[i]), 3)})
             speedups.append(sp)
         if model_ms is not None and c["model"]:
             e.update({"model_plan_GBps": round(c["bytes"] / (model_ms[i] * 1e-3) / 1e9, 1),
@@ -582,6 +604,8 @@ def main():
             "l2": "flushed before every config (256 MiB write, then a 256 MiB read so no dirty lines remain); flush outside the timed CUDA-event intervals",
             "shared_limit_bytes": W.B200_SHARED_LIMIT,
             "geomean_speedup_vs_unfused": geo,
+            "geomean_speedup_vs_unfused_folded": (float(math.exp(np.mean(np.log([v["speedup_vs_unfused_folded"] for v in suite.values()]))))
+                                                   if base_ms is not None else None),
             "suite": suite,
         },
         "roofline": {"bound": "hbm", "kernel": "%s/%s" % (cfg_name, kname), "achieved": achieved, "peak": peak,
