@@ -2094,49 +2094,70 @@ void Builder::emit_row_finalize(std::vector<Component*>& comps) {
   if (!any) return;
   uses_barrier_ = true;
   ln("stitch_dev::grid_barrier(gsync);");
-  ln("// deterministic combine of the per-CTA partials");
+  ln("// deterministic combine of the per-CTA partials: every (output, column");
+  ln("// block) item of every cross output in ONE grid-stride loop, so all CTAs");
+  ln("// work at once (not one output after another on So / 32 CTAs)");
+  struct Item {
+    int x;
+    int64_t So;
+    int CW;
+    int64_t first, count;
+  };
+  std::vector<Item> items;
+  int64_t total = 0;
   for (Component* c : comps)
     for (int x : c->cross) {
       const OpNode& op = *vals_[x].node;
       const int in = vals_[x].operands[0];
       bool scalar = static_cast<int>(op.reduce_dims.size()) == static_cast<int>(vals_[in].dims.size());
       const int64_t So = scalar ? 1 : prod(vals_[in].dims, c->k);
-      const std::string Op = op.elem_name == "max" ? "stitch_dev::MaxOp" : "stitch_dev::SumOp";
-      // Parallel fixed-order combine: a CTA owns a block of CW columns, its
-      // threads split the partial rows (slice s of S), then slice 0 joins
-      // the S slice sums in order through shared memory.
       const int CW = So >= 32 ? 32 : 1;
-      open("");
-      ln("const int CW = " + std::to_string(CW) + ", S = blockDim.x / CW;");
-      ln("const int c = threadIdx.x % CW, s = threadIdx.x / CW;");
-      open("for (long long cb = blockIdx.x; cb * CW < " + std::to_string(So) + "LL; cb += gridDim.x)");
-      ln("const long long i = cb * CW + c;");
-      ln("float a = " + Op + "::init();");
-      ln("if (i < " + std::to_string(So) + "LL) a = stitch_dev::combine_strided<" + Op + ">(ws + " +
-         std::to_string(ws_off_[x]) + "LL, " + cross_parts_[x] + ", " + std::to_string(So) + "LL, i, s, S);");
-      ln("__syncthreads();");
-      ln("smem[s * CW + c] = a;");
-      ln("__syncthreads();");
-      if (CW == 1) {
-        // scalar: warp 0 folds the slices (lane l: slices l, l+32, ...) and
-        // finishes with a fixed xor-shuffle tree
-        open("if (threadIdx.x < 32)");
-        ln("float v = " + Op + "::init();");
-        ln("for (int j = threadIdx.x; j < S; j += 32) v = " + Op + "::apply(v, smem[j]);");
-        ln("v = stitch_dev::warp_allreduce<" + Op + ">(v);");
-        open("if (threadIdx.x == 0)");
-      } else {
-        open("if (s == 0 && i < " + std::to_string(So) + "LL)");
-        ln("float v = " + Op + "::init();");
-        ln("for (int j = 0; j < S; ++j) v = " + Op + "::apply(v, smem[j * CW + c]);");
-      }
-      if (vals_[x].output) ln(out_ptr(x) + "[i] = v;");
-      if (materialized_.count(x) && !vals_[x].output) ln(materialized_[x] + "[i] = v;");
-      close();
-      if (CW == 1) close();
-      close();
-      close();
+      const int64_t cnt = (So + CW - 1) / CW;
+      items.push_back({x, So, CW, total, cnt});
+      total += cnt;
     }
+  open("for (long long item = blockIdx.x; item < " + std::to_string(total) + "LL; item += gridDim.x)");
+  for (size_t j = 0; j < items.size(); ++j) {
+    const Item& it = items[j];
+    const int x = it.x;
+    const OpNode& op = *vals_[x].node;
+    const int64_t So = it.So;
+    const int CW = it.CW;
+    const std::string Op = op.elem_name == "max" ? "stitch_dev::MaxOp" : "stitch_dev::SumOp";
+    // Parallel fixed-order combine: a CTA owns a block of CW columns, its
+    // threads split the partial rows (slice s of S), then slice 0 joins
+    // the S slice sums in order through shared memory.
+    open(std::string(j ? "else " : "") + "if (item < " + std::to_string(it.first + it.count) + "LL)");
+    ln("const long long cb = item - " + std::to_string(it.first) + "LL;");
+    ln("const int CW = " + std::to_string(CW) + ", S = blockDim.x / CW;");
+    ln("const int c = threadIdx.x % CW, s = threadIdx.x / CW;");
+    ln("const long long i = cb * CW + c;");
+    ln("float a = " + Op + "::init();");
+    ln("if (i < " + std::to_string(So) + "LL) a = stitch_dev::combine_strided<" + Op + ">(ws + " +
+       std::to_string(ws_off_[x]) + "LL, " + cross_parts_[x] + ", " + std::to_string(So) + "LL, i, s, S);");
+    ln("__syncthreads();");
+    ln("smem[s * CW + c] = a;");
+    ln("__syncthreads();");
+    if (CW == 1) {
+      // scalar: warp 0 folds the slices (lane l: slices l, l+32, ...) and
+      // finishes with a fixed xor-shuffle tree
+      open("if (threadIdx.x < 32)");
+      ln("float v = " + Op + "::init();");
+      ln("for (int j = threadIdx.x; j < S; j += 32) v = " + Op + "::apply(v, smem[j]);");
+      ln("v = stitch_dev::warp_allreduce<" + Op + ">(v);");
+      open("if (threadIdx.x == 0)");
+    } else {
+      open("if (s == 0 && i < " + std::to_string(So) + "LL)");
+      ln("float v = " + Op + "::init();");
+      ln("for (int j = 0; j < S; ++j) v = " + Op + "::apply(v, smem[j * CW + c]);");
+    }
+    if (vals_[x].output) ln(out_ptr(x) + "[i] = v;");
+    if (materialized_.count(x) && !vals_[x].output) ln(materialized_[x] + "[i] = v;");
+    close();
+    if (CW == 1) close();
+    close();
+  }
+  close();
   bool any_post = false;
   for (Component* c : comps) any_post = any_post || !c->post.empty();
   if (!any_post) return;
@@ -2914,8 +2935,9 @@ KernelSpec Builder::build() {
     for (size_t i = 0; i < vals_[m].operands.size(); ++i) head << (i ? ", " : "") << vals_[vals_[m].operands[i]].id;
     head << ")\n";
   }
-  head << "extern \"C\" __global__ void __launch_bounds__(" << block << ") " << name_ << "(" << join(params, ", ")
-       << ") {\n";
+  head << "extern \"C\" __global__ void __launch_bounds__(" << block
+       << (opts_.min_ctas_per_sm > 0 ? ", " + std::to_string(opts_.min_ctas_per_sm) : std::string()) << ") " << name_ << "("
+       << join(params, ", ") << ") {\n";
   head << "  extern __shared__ __align__(128) float smem[];\n";
   // Programmatic dependent launch: this grid may be scheduled while the
   // previous kernel drains; wait for it (and its memory) before touching any

@@ -89,6 +89,8 @@ struct CodegenOptions {
   // (the GRU group): the warp-specialised tcgen05 scheme (device gws::run,
   // TMA producer / MMA issuer / split / tail warps). Off: the ROW scheme.
   bool gws = true;
+  // __launch_bounds__ minimum CTAs per SM (register budget hint; 0: none)
+  int min_ctas_per_sm = 0;
   // Groups ROW / COLRED / FLAT cannot take (dots + reductions over different
   // index spaces, paper Fig. 1) run as BLOCK composition -- one CTA per
   // leading index, shared memory at the planner's Alg. 4 alloc map -- instead

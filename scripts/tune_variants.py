@@ -31,6 +31,9 @@ VARIANTS = [
     {"wide_cross_cta": True},
     {"wide_cross_cta": True, "wide_cross_threads": 128},
     {"wide_cross_cta": True, "wide_cross_threads": 384},
+    {"wide_cross_cta": True, "wide_cross_threads": 192},
+    {"wide_cross_cta": True, "wide_cross_threads": 256},
+    {"lazy_inputs": True, "cross_smem": False},
     {"cross_smem": False},
     {"row_prefetch_warp": True},
     {"row_prefetch": False},
@@ -50,7 +53,7 @@ def main():
     from paper_1911_11576_b200 import runtime as rt
     ap = argparse.ArgumentParser()
     ap.add_argument("config")
-    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--reps", type=int, default=9)
     ap.add_argument("--min-gain", type=float, default=0.03)
     ap.add_argument("--out", default="")
     a = ap.parse_args()
