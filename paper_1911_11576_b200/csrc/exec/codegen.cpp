@@ -107,6 +107,7 @@ struct Component {
   int64_t cr_R = 0, cr_C = 0, cr_ncb = 0, cr_nch = 0, cr_rpc = 0;
   int cr_sync = 0, cr_m = -1, cr_w = 128;
   int cr_cluster = 0;         // COLRED: row chunks of a column block form a cluster of this many CTAs
+  std::vector<int> cr_eouts;  // COLRED: elementwise outputs written from the same tiles
   bool tc = false;            // gemm stages on tcgen05 (3xTF32): smem scratch + TMEM accumulator
   int tc_k = 0;               // largest K among the tensor-core gemm stages
   std::vector<char> tc_dot;   // value -> gemm stage runs on tcgen05
@@ -364,11 +365,19 @@ bool Builder::plan_colred(Component& c) {
     if (xo.type == OpType::kReduce) {
       if (m >= 0) return false;
       m = x;
-    } else if (xo.type != OpType::kElementwise || vals_[x].output) {
+    } else if (xo.type != OpType::kElementwise) {
       return false;
     }
   }
   if (m < 0 || !vals_[m].output) return false;
+  // elementwise outputs over the reduce input's index space (e.g. the GeLU
+  // backward dx beside its bias gradient) are written from the same tiles
+  c.cr_eouts.clear();
+  for (int x : c.members)
+    if (x != m && vals_[x].output) {
+      if (!opts_.colred_eout || vals_[x].dims != vals_[vals_[m].operands[0]].dims) return false;
+      c.cr_eouts.push_back(x);
+    }
   if (c.members.size() > 1 && !opts_.colred_fused) return false;
   const OpNode& op = *vals_[m].node;
   const int in = vals_[m].operands[0];
@@ -453,6 +462,7 @@ void Builder::emit_colred(Component& c, const std::string& lo, const std::string
       for (int o : vals_[v].operands) walk(o);
   };
   walk(in);
+  for (int eo : c.cr_eouts) walk(eo);
   if (opts_.colred_cp_async)
     iters = std::max<int64_t>(1, std::min<int64_t>(iters, kColredStageSlots / std::max<int64_t>(1, static_cast<int64_t>(ins.size()))));
   const std::string IT = std::to_string(iters);
@@ -504,6 +514,11 @@ void Builder::emit_colred(Component& c, const std::string& lo, const std::string
         memo_.back()[std::to_string(v) + "@" + join(coords(u), ",")] = qname[v] + (cpa ? "" : "[i]") + lanes[u];
     std::vector<std::string> xv;
     for (int u = 0; u < 4; ++u) xv.push_back(at(in, coords(u)));
+    for (int eo : c.cr_eouts) {
+      std::vector<std::string> ev;
+      for (int u = 0; u < 4; ++u) ev.push_back(at(eo, coords(u)));
+      ln("stitch_dev::st4(" + out_ptr(eo) + " + r * " + C + " + col, " + ev[0] + ", " + ev[1] + ", " + ev[2] + ", " + ev[3] + ");");
+    }
     memo_.pop_back();
     ln("a0 = " + Op + "::apply(a0, " + xv[0] + "); a1 = " + Op + "::apply(a1, " + xv[1] + "); a2 = " + Op + "::apply(a2, " +
        xv[2] + "); a3 = " + Op + "::apply(a3, " + xv[3] + ");");

@@ -104,7 +104,12 @@ struct CodegenOptions {
   // many CTAs, combined through distributed shared memory (cluster barrier
   // + DSMEM loads, fixed rank order) instead of global partials + fence +
   // arrival counter + last-CTA fold; 0: the global scheme
-  int colred_cluster = 16;  // BERT step 2.257 -> 2.195 ms (8: 2.205; 2: 2.473)
+  int colred_cluster = 16;
+  // COLRED also for groups whose other outputs are elementwise over the
+  // reduce input's [R, C] (written from the same tiles). Off by default:
+  // measured slower than CTA rows on BERT's [4096, 3072] GeLU-backward groups
+  // (step 2.111 -> 2.433 ms); a per-group tuning candidate.
+  bool colred_eout = false;  // BERT step 2.257 -> 2.195 ms (8: 2.205; 2: 2.473)
   int colred_cols = 32;        // COLRED column-block width: 32, 64 or 128 floats (32: BERT 2387 -> 2375 us)
   bool colred_cp_async = true;  // COLRED loads staged through cp.async (all of a pass in flight)  // COLRED also for reduces of an inline elementwise producer chain
   // many-input rows: load inputs per fused-loop step, not per row (measured

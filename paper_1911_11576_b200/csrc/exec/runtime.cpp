@@ -123,6 +123,7 @@ void apply_codegen_options(CodegenOptions& c, const json::Value& o) {
   if (o.has("colred_cols")) c.colred_cols = static_cast<int>(o.at("colred_cols").as_int());
   if (o.has("colred_ctas_per_sm")) c.colred_ctas_per_sm = static_cast<int>(o.at("colred_ctas_per_sm").as_int());
   if (o.has("colred_cluster")) c.colred_cluster = static_cast<int>(o.at("colred_cluster").as_int());
+  if (o.has("colred_eout")) c.colred_eout = o.at("colred_eout").as_bool();
   if (o.has("loop_fusion")) c.loop_fusion = o.at("loop_fusion").as_bool();
   if (o.has("row_prefetch")) c.row_prefetch = o.at("row_prefetch").as_bool();
   if (o.has("tma_double_buffer")) c.tma_double_buffer = o.at("tma_double_buffer").as_bool();

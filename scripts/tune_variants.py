@@ -43,6 +43,9 @@ VARIANTS = [
     {"colred_cols": 128},
     {"colred_cluster": 8},
     {"colred_cluster": 0},
+    {"colred_eout": True},
+    {"colred_eout": True, "colred_cluster": 0},
+    {"colred_eout": True, "colred_cols": 128},
     {"pack_sequential": True},
     {"tma_double_buffer": True},
 ]

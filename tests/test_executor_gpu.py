@@ -576,3 +576,30 @@ def test_broadcast_sinking_parity():
     for x, y in zip(a, b):
         assert np.array_equal(x, y)
     assert_parity(g, g, ins, fold_constants=False)
+
+
+@pytest.mark.parametrize("R,C", [(64, 768), (4096, 3072), (1000, 132), (37, 4)])
+@pytest.mark.parametrize("opts", [{"colred_eout": True}, {"colred_eout": True, "colred_cluster": 0},
+                                  {"colred_eout": True, "colred_cp_async": False}], ids=["cluster", "global", "ldg"])
+def test_colred_with_elementwise_outputs(R, C, opts):
+    """COLRED groups whose other outputs are elementwise over the reduce
+    input (the GeLU-backward dx beside its bias gradient): the elementwise
+    outputs are written from the same tiles; oracle parity and bit-identical
+    reruns."""
+    g = {"nodes": [{"id": "dy", "kind": "parameter", "shape": {"dims": [R, C], "dtype": "f32"}},
+                   {"id": "x", "kind": "parameter", "shape": {"dims": [R, C], "dtype": "f32"}},
+                   {"id": "e", "kind": "elementwise", "name": "exp", "operands": ["x"], "shape": {"dims": [R, C], "dtype": "f32"}},
+                   {"id": "dx", "kind": "elementwise", "name": "multiply", "operands": ["dy", "e"],
+                    "shape": {"dims": [R, C], "dtype": "f32"}},
+                   {"id": "db", "kind": "reduce", "operands": ["dx"], "reduce_dims": [0], "shape": {"dims": [C], "dtype": "f32"}},
+                   {"id": "t", "kind": "tuple", "operands": ["dx", "db"], "shape": {"dims": [C], "dtype": "f32"}}],
+         "outputs": ["t"]}
+    fused = rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT)["fused"]
+    ins = orc.random_inputs(g, seed=R + 3 * C, scale=0.5)
+    ex = assert_parity(g, fused, ins, **opts)
+    if C % 4 == 0:
+        assert "colred" in ex.info["kernels"][0]["scheme"], ex.info["kernels"]
+    _, a = run_device(fused, ins, **opts)
+    _, b = run_device(fused, ins, **opts)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
