@@ -603,3 +603,36 @@ def test_colred_with_elementwise_outputs(R, C, opts):
     _, b = run_device(fused, ins, **opts)
     for x, y in zip(a, b):
         assert np.array_equal(x, y)
+
+
+def test_parity_margins_report():
+    """The achieved margins, not just pass/fail: for every suite config's
+    SMALL size (model plan at both shared limits and unfused) each output's
+    worst err / tol, max and median err / (1e-5 base), and median tol / base,
+    written to gpurun_out/parity_margins.json when that directory exists."""
+    import json
+    import os
+    rows = []
+    for name in W.CONFIGS:
+        g = W.CONFIGS[name](**W.SMALL[name])
+        ins = orc.random_inputs(g, seed=17, scale=0.5 if name == "bert" else 1.0)
+        ref, bound = tolerance.reference_with_bound(g, ins)
+        for tag, fused in (("b200", rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT)["fused"]),
+                           ("ref48k", rt.plan(g, shared_limit_bytes=W.REFERENCE_SHARED_LIMIT)["fused"]), ("unfused", g)):
+            _, got = run_device(fused, ins)
+            for oid, a, r, b in zip(orc.graph_outputs(g), got, ref, bound):
+                a = a.astype(np.float64).reshape(r.shape)
+                base = np.maximum(tolerance.RTOL * np.abs(r), tolerance.ATOL)
+                tol = base + tolerance.SAFETY * np.nan_to_num(b, nan=np.inf, posinf=np.inf)
+                fin = np.isfinite(tol)
+                err = np.abs(a - r)
+                ok, worst = tolerance.check(a, r, b)
+                assert ok, (name, tag, oid, worst)
+                rows.append({"config": name, "plan": tag, "output": oid, "elements": int(r.size),
+                             "uncertified": int((~fin).sum()), "worst_err_over_tol": worst,
+                             "max_err_over_base": float(np.max(err / base)),
+                             "median_err_over_base": float(np.median(err / base)),
+                             "median_tol_over_base": float(np.median(tol[fin] / base[fin])) if fin.any() else None})
+    if os.path.isdir("gpurun_out"):
+        with open("gpurun_out/parity_margins.json", "w") as f:
+            json.dump(rows, f, indent=1)
