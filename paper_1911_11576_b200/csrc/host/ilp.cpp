@@ -63,7 +63,12 @@ std::vector<double> lp_node_prices(const std::vector<std::vector<int>>& sets, co
   std::vector<std::vector<int>> col(n);
   for (int j = 0; j < n; ++j)
     for (int x : sets[j]) col[j].push_back(row_of[x]);
+  // Right-hand side perturbed per row (1 + 1e-7 .. 2e-7): set-packing LPs
+  // are massively primal-degenerate and the unperturbed simplex stalls for
+  // hundreds of thousands of pivots; on the perturbed one every ratio test
+  // makes progress. The final basis is re-evaluated on the true b = 1.
   std::vector<double> Binv(static_cast<size_t>(m) * m, 0.0), xb(m, 1.0), cb(m, 0.0), dual(m, 0.0), d(m);
+  for (int i = 0; i < m; ++i) xb[i] = 1.0 + 1e-7 * (1.0 + ((i * 2654435761u) % 1024) / 1024.0);
   for (int i = 0; i < m; ++i) Binv[static_cast<size_t>(i) * m + i] = 1.0;
   std::vector<int> basis(m);
   for (int i = 0; i < m; ++i) basis[i] = n + i;  // slacks
@@ -72,7 +77,8 @@ std::vector<double> lp_node_prices(const std::vector<std::vector<int>>& sets, co
   bool optimal = false;
   // Iteration cap: degenerate whole-graph LPs can pivot for a long time; on
   // a miss the max-ratio prices (weaker, still valid) are used instead.
-  for (int iter = 0; iter < 8 * m + 2000; ++iter) {
+  int lp_iters = 0;
+  for (int iter = 0; iter < 20 * m + 2000; ++iter, ++lp_iters) {
     // duals: dual = cb^T Binv
     for (int k = 0; k < m; ++k) dual[k] = 0.0;
     for (int i = 0; i < m; ++i)
@@ -133,15 +139,23 @@ std::vector<double> lp_node_prices(const std::vector<std::vector<int>>& sets, co
     basis[r] = e;
     cb[r] = e < n ? s[e] : 0.0;
   }
+  if (std::getenv("STITCH_ILP_TRACE"))
+    std::fprintf(stderr, "[ilp]   LP m=%d n=%d iterations=%d optimal=%d\n", m, n, lp_iters, (int)optimal);
   if (!optimal) {
     ratio_prices();
     return y;
   }
   for (int k = 0; k < m; ++k) y[rows[k]] = std::max(0.0, dual[k]);
   if (primal) {
+    // primal values of the optimal basis for b = 1
     primal->assign(n, 0.0);
-    for (int i = 0; i < m; ++i)
-      if (basis[i] < n) (*primal)[basis[i]] = xb[i];
+    for (int i = 0; i < m; ++i) {
+      if (basis[i] >= n) continue;
+      const double* bi = &Binv[static_cast<size_t>(i) * m];
+      double xi = 0.0;
+      for (int k = 0; k < m; ++k) xi += bi[k];
+      (*primal)[basis[i]] = xi;
+    }
   }
   // repair: make every pattern constraint hold (with a relative margin)
   for (int j = 0; j < n; ++j) {
@@ -156,9 +170,58 @@ std::vector<double> lp_node_prices(const std::vector<std::vector<int>>& sets, co
   return y;
 }
 
+// Near-optimality window delta: every selection S whose canonical total can
+// equal the canonical optimum has a real total within delta of the real
+// optimum R*. Recursive summation of k >= 0 terms errs by at most
+// gamma_{k-1} * sum (gamma_k = k u / (1 - k u), u = 2^-53), so
+// canonical(S) >= canonical(S*) >= R*(1 - gamma) and
+// canonical(S) <= R(S)(1 + gamma) give R(S) >= R* - 2 gamma R*; the window
+// is 8 gamma_K R_up (4x headroom for the approximate running totals the
+// search compares), with K the largest possible selection (node-disjoint
+// patterns: at most one per covered node) and R_up the fractional
+// node-price bound sum_x max_{P covers x} s_P / |P| >= R*.
+double selection_window(const IlpInstance& inst) {
+  const int n = inst.num_vars;
+  const bool nodes = static_cast<int>(inst.node_sets.size()) == n && inst.num_nodes > 0;
+  double rup = 0.0;
+  long long k = 0;
+  if (nodes) {
+    std::vector<double> best(inst.num_nodes, 0.0);
+    std::vector<char> used(inst.num_nodes, 0);
+    for (int v = 0; v < n; ++v) {
+      if (inst.scores[v] <= 0.0) continue;
+      if (inst.node_sets[v].empty()) {
+        rup += inst.scores[v];
+        ++k;
+        continue;
+      }
+      const double r = inst.scores[v] / inst.node_sets[v].size();
+      for (int x : inst.node_sets[v]) {
+        best[x] = std::max(best[x], r);
+        used[x] = 1;
+      }
+    }
+    for (int x = 0; x < inst.num_nodes; ++x) {
+      rup += best[x] * (1.0 + 1e-12);
+      k += used[x];
+    }
+  } else {
+    for (double sv : inst.scores)
+      if (sv > 0.0) {
+        rup += sv;
+        ++k;
+      }
+  }
+  const double u = std::ldexp(1.0, -53);
+  const double kk = static_cast<double>(k + 2);
+  const double gamma = kk * u / (1.0 - kk * u);
+  return 8.0 * gamma * rup * (1.0 + 1e-9);
+}
+
 class Search {
  public:
-  explicit Search(const IlpInstance& inst) : in_(inst), n_(inst.num_vars) {
+  explicit Search(const IlpInstance& inst, double window = -1.0)
+      : in_(inst), n_(inst.num_vars), window_(window >= 0.0 ? window : selection_window(inst)) {
     // Conflicts either as explicit pairs or implied by shared graph nodes
     // (planner instances: pair lists grow quadratically with overlap).
     node_mode_ = inst.pairs.empty() && static_cast<int>(inst.node_sets.size()) == n_ && inst.num_nodes > 0;
@@ -207,8 +270,19 @@ class Search {
           if (inst.scores[v] > 0.0 && !inst.node_sets[v].empty()) {
             const double xv = xlp[k2++];
             if (xv > 1e-7 && xv < 1.0 - 1e-7) integral = false;
+            else if (xv < -1e-7 || xv > 1.0 + 1e-7) integral = false;
             else if (xv >= 0.5) inc.push_back(v);
           }
+        // the incumbent must be a feasible packing (the LP basis was chosen on
+        // a perturbed right-hand side)
+        if (integral) {
+          std::vector<char> hit(inst.num_nodes, 0);
+          for (int v : inc)
+            for (int x : inst.node_sets[v]) {
+              if (hit[x]) integral = false;
+              hit[x] = 1;
+            }
+        }
         if (integral) {
           std::vector<int> cc(inst.cycles.size(), 0);
           for (int v : inc)
@@ -220,16 +294,39 @@ class Search {
             if (cc[c] > static_cast<int>(inst.cycles[c].pattern_indices.size()) - 1) integral = false;
         }
         if (integral) {
-          double incumbent = 0.0, total = 0.0;
+          // r_j x_j summed over a selection within the window of the
+          // incumbent is at least -(ysum - incumbent + window); the
+          // floating-point error of ysum, the incumbent and each r_j is
+          // below (m + |P| + k + 3) eps (ysum + s_P), covered 4x.
+          double incumbent = 0.0;
           for (int v : inc) incumbent += inst.scores[v];
-          for (double sv : inst.scores) total += sv;
-          const double margin = (ysum - incumbent) + 16.0 * (n_ + 2) * std::numeric_limits<double>::epsilon() * total + 1e-9;
+          size_t maxp = 0;
+          for (int v = 0; v < n_; ++v) maxp = std::max(maxp, inst.node_sets[v].size());
+          const double eps = std::numeric_limits<double>::epsilon();
+          const double fp = 4.0 * (inst.num_nodes + maxp + inc.size() + 3) * eps * 2.0 * (ysum + 1.0);
+          const double margin = (ysum - incumbent) + window_ + fp;
           rc_out_.assign(n_, 0);
           for (int v = 0; v < n_; ++v) {
             if (inst.scores[v] <= 0.0 || inst.node_sets[v].empty()) continue;
             double r = inst.scores[v];
             for (int x : inst.node_sets[v]) r -= lp_price_[x];
             if (r < -margin) rc_out_[v] = 1;
+          }
+        }
+        if (const char* rp = std::getenv("STITCH_ILP_REDUCED")) {
+          // the variables reduced-cost fixing keeps, with their node sets and
+          // reduced costs, and the node prices (solver development aid)
+          if (FILE* f = std::fopen(rp, "w")) {
+            for (int v = 0; v < n_; ++v) {
+              if (inst.scores[v] <= 0.0 || inst.node_sets[v].empty() || (!rc_out_.empty() && rc_out_[v])) continue;
+              double r = inst.scores[v];
+              for (int x : inst.node_sets[v]) r -= lp_price_[x];
+              std::fprintf(f, "v %d %a %a", v, inst.scores[v], r);
+              for (int x : inst.node_sets[v]) std::fprintf(f, " %d", x);
+              std::fprintf(f, "\n");
+            }
+            for (int x = 0; x < inst.num_nodes; ++x) std::fprintf(f, "y %d %a\n", x, lp_price_[x]);
+            std::fclose(f);
           }
         }
         if (std::getenv("STITCH_ILP_TRACE")) {
@@ -262,8 +359,16 @@ class Search {
     words_ = (n_ + 63) / 64;
     double total = 0.0;
     for (double s : inst.scores) total += s;
-    // Relative slack covering the rounding of any partial sum of <= n terms.
-    slack_ = 4.0 * (n_ + 2) * std::numeric_limits<double>::epsilon();
+    // Relative slack covering the rounding of any partial sum the search
+    // forms: <= n terms in general; with node sets and the node clique hint
+    // every sum (selection, clique cover, node prices) has at most one term
+    // per graph node (+ the patterns covering none).
+    long long terms = n_;
+    if (use_frac_ && static_cast<int>(inst.clique_hint.size()) == n_) {
+      terms = inst.num_nodes;
+      for (int v = 0; v < n_; ++v) terms += inst.node_sets[v].empty() ? 1 : 0;
+    }
+    slack_ = 4.0 * (terms + 2) * std::numeric_limits<double>::epsilon();
     (void)total;
   }
 
@@ -304,6 +409,9 @@ class Search {
   }
 
   bool in_best(int v) const { return (best_bits_[v >> 6] >> (v & 63)) & 1; }
+  // Variables reduced-cost fixing proved absent from every selection within
+  // the window of the optimum (empty when the LP was not integral).
+  const std::vector<char>& fixed_out() const { return rc_out_; }
 
   // Every feasible selection of positive-score variables whose total is
   // within `delta` of the optimum (approximate totals; the caller re-sums
@@ -514,8 +622,11 @@ class Search {
           int v = free_[i];
           if (!takeable(v)) continue;
           avail_[v] = avail_stamp_;
+          // every node of every available pattern (not only those the
+          // early-exiting static pass above reached: a pattern's constraint
+          // must see current prices on all of its nodes)
           for (int x : in_.node_sets[v])
-            if (lp_stamp_[x] == stamp_ && ystamp_[x] != avail_stamp_) {
+            if (ystamp_[x] != avail_stamp_) {
               ystamp_[x] = avail_stamp_;
               y_[x] = lp_price_[x];
               cov.push_back(x);
@@ -553,6 +664,7 @@ class Search {
 
   const IlpInstance& in_;
   int n_;
+  double window_;
   std::vector<std::vector<int>> adj_;
   std::vector<int> limit_;
   std::vector<std::vector<int>> cycles_of_;
@@ -666,41 +778,98 @@ bool solve_decomposed(const IlpInstance& inst, FusionPlan* plan) {
     comps[find(v)].push_back(v);
     total += inst.scores[v];
   }
-  const double delta = 8.0 * (n + 2) * std::numeric_limits<double>::epsilon() * std::max(total, 1e-300);
+  (void)total;
+  const double delta = selection_window(inst);
 
   // Near-optimal selections per component (global indices).
   std::vector<std::vector<std::vector<int>>> per;
-  for (auto& [root, vars] : comps) {
-    (void)root;
-    bool any_pos = false;
-    for (int v : vars) any_pos = any_pos || inst.scores[v] > 0.0;
-    if (!any_pos) continue;
+  static const bool trace = std::getenv("STITCH_ILP_TRACE") != nullptr;
+  // Sub-instance over `vars` (global indices, ascending).
+  auto restrict_to = [&](const std::vector<int>& vars) {
     std::map<int, int> local;
     for (size_t i = 0; i < vars.size(); ++i) local[vars[i]] = static_cast<int>(i);
     IlpInstance sub;
     sub.num_vars = static_cast<int>(vars.size());
     for (int v : vars) sub.scores.push_back(inst.scores[v]);
     for (const PairConstraint& pc : inst.pairs)
-      if (local.count(pc.u)) sub.pairs.push_back({local[pc.u], local[pc.v]});
-    for (const CycleConstraint& cc : inst.cycles)
-      if (local.count(cc.pattern_indices[0])) {
-        CycleConstraint c2;
-        for (int v : cc.pattern_indices) c2.pattern_indices.push_back(local[v]);
-        sub.cycles.push_back(c2);
-      }
+      if (local.count(pc.u) && local.count(pc.v)) sub.pairs.push_back({local[pc.u], local[pc.v]});
+    // a cycle constraint with a member outside `vars` (fixed to 0) holds
+    for (const CycleConstraint& cc : inst.cycles) {
+      bool all = true;
+      for (int v : cc.pattern_indices) all = all && local.count(v);
+      if (!all) continue;
+      CycleConstraint c2;
+      for (int v : cc.pattern_indices) c2.pattern_indices.push_back(local[v]);
+      sub.cycles.push_back(c2);
+    }
     if (static_cast<int>(inst.clique_hint.size()) == n)
       for (int v : vars) sub.clique_hint.push_back(inst.clique_hint[v]);
     if (static_cast<int>(inst.node_sets.size()) == n) {
       sub.num_nodes = inst.num_nodes;
       for (int v : vars) sub.node_sets.push_back(inst.node_sets[v]);
     }
-    static const bool trace = std::getenv("STITCH_ILP_TRACE") != nullptr;
-    if (trace) std::fprintf(stderr, "[ilp] solving component vars=%zu\n", vars.size());
+    return sub;
+  };
+  // Collects the component's near-optimal selections into `per`; false when
+  // a cap or the node budget trips.
+  std::function<bool(const std::vector<int>&, int)> collect = [&](const std::vector<int>& vars, int depth) -> bool {
+    bool any_pos = false;
+    for (int v : vars) any_pos = any_pos || inst.scores[v] > 0.0;
+    if (!any_pos) return true;
+    IlpInstance sub = restrict_to(vars);
+    if (trace) std::fprintf(stderr, "[ilp] %*ssolving component vars=%zu\n", 2 * depth, "", vars.size());
     const auto tc0 = std::chrono::steady_clock::now();
-    Search search(sub);
+    Search search(sub, delta);
     if (trace)
       std::fprintf(stderr, "[ilp]   setup+LP %.2fs\n",
                    std::chrono::duration<double>(std::chrono::steady_clock::now() - tc0).count());
+    // Reduced-cost fixing leaves only the variables a near-optimal selection
+    // can use; those often fall apart into independent pieces (an LP with
+    // many zero-reduced-cost columns), and searching the pieces jointly
+    // multiplies their trees. Split and collect each piece on its own (the
+    // window applies per piece for the same reason it applies per
+    // component); the combination step below takes their product.
+    const std::vector<char>& out = search.fixed_out();
+    if (!out.empty() && depth < 32) {
+      std::vector<int> kept;
+      for (size_t i = 0; i < vars.size(); ++i)
+        if (!out[i]) kept.push_back(vars[i]);
+      std::vector<int> par(kept.size());
+      std::iota(par.begin(), par.end(), 0);
+      std::function<int(int)> fd = [&](int x) { return par[x] == x ? x : par[x] = fd(par[x]); };
+      std::map<int, int> pos;
+      for (size_t i = 0; i < kept.size(); ++i) pos[kept[i]] = static_cast<int>(i);
+      if (node_mode || static_cast<int>(inst.node_sets.size()) == n) {
+        std::map<int, int> owner;
+        for (size_t i = 0; i < kept.size(); ++i)
+          for (int x : inst.node_sets[kept[i]]) {
+            auto it = owner.emplace(x, static_cast<int>(i)).first;
+            par[fd(static_cast<int>(i))] = fd(it->second);
+          }
+      }
+      for (const PairConstraint& pc : inst.pairs)
+        if (pos.count(pc.u) && pos.count(pc.v)) par[fd(pos[pc.u])] = fd(pos[pc.v]);
+      for (const CycleConstraint& cc : inst.cycles) {
+        bool all = true;
+        for (int v : cc.pattern_indices) all = all && pos.count(v);
+        if (all)
+          for (size_t i = 1; i < cc.pattern_indices.size(); ++i)
+            par[fd(pos[cc.pattern_indices[i]])] = fd(pos[cc.pattern_indices[0]]);
+      }
+      std::map<int, std::vector<int>> pieces;
+      for (size_t i = 0; i < kept.size(); ++i) pieces[fd(static_cast<int>(i))].push_back(kept[i]);
+      // recurse while the pieces shrink: a fresh LP over fewer columns fixes
+      // more of them
+      if (pieces.size() > 1 || kept.size() < vars.size()) {
+        if (trace)
+          std::fprintf(stderr, "[ilp]   reduced to %zu variables in %zu pieces\n", kept.size(), pieces.size());
+        for (auto& [r, pv] : pieces) {
+          (void)r;
+          if (!collect(pv, depth + 1)) return false;
+        }
+        return true;
+      }
+    }
     search.node_budget_ = ilp_node_budget();
     std::vector<std::vector<int>> cands;
     const long long n0 = g_stats.nodes;
@@ -713,12 +882,18 @@ bool solve_decomposed(const IlpInstance& inst, FusionPlan* plan) {
       g_stats.lp_gap += std::max(0.0, search.lp_bound_ - inc);
     }
     if (trace)
-      std::fprintf(stderr, "[ilp] component vars=%zu candidates=%zu nodes=%lld%s%s\n", vars.size(), cands.size(),
-                   g_stats.nodes - n0, ok ? "" : " (cap: fallback)", search.truncated_ ? " (node budget: incumbent)" : "");
+      std::fprintf(stderr, "[ilp] %*scomponent vars=%zu candidates=%zu nodes=%lld%s%s\n", 2 * depth, "", vars.size(),
+                   cands.size(), g_stats.nodes - n0, ok ? "" : " (cap: fallback)",
+                   search.truncated_ ? " (node budget: incumbent)" : "");
     if (!ok) return false;
     for (auto& c : cands)
       for (int& v : c) v = vars[v];
     per.push_back(std::move(cands));
+    return true;
+  };
+  for (auto& [root, vars] : comps) {
+    (void)root;
+    if (!collect(vars, 0)) return false;
   }
   // Canonical optimum over the combinations.
   size_t combos = 1;
@@ -821,6 +996,34 @@ bool solve_decomposed(const IlpInstance& inst, FusionPlan* plan) {
   return true;
 }
 
+// STITCH_ILP_DUMP=<prefix>: every instance solved is written to
+// <prefix>.<k>.txt (scores as hex floats, node sets, pairs, cycles) for the
+// offline solver driver scripts/probes/ilp_driver.cpp.
+void dump_instance(const IlpInstance& inst) {
+  static const char* prefix = std::getenv("STITCH_ILP_DUMP");
+  if (!prefix) return;
+  static int k = 0;
+  const std::string path = std::string(prefix) + "." + std::to_string(k++) + ".txt";
+  FILE* f = std::fopen(path.c_str(), "w");
+  if (!f) return;
+  std::fprintf(f, "%d %d %zu %zu %zu\n", inst.num_vars, inst.num_nodes, inst.pairs.size(), inst.cycles.size(),
+               inst.clique_hint.size());
+  for (double s : inst.scores) std::fprintf(f, "%a\n", s);
+  for (int v = 0; v < inst.num_vars && inst.num_nodes > 0; ++v) {
+    std::fprintf(f, "%zu", inst.node_sets[v].size());
+    for (int x : inst.node_sets[v]) std::fprintf(f, " %d", x);
+    std::fprintf(f, "\n");
+  }
+  for (const PairConstraint& pc : inst.pairs) std::fprintf(f, "%d %d\n", pc.u, pc.v);
+  for (const CycleConstraint& cc : inst.cycles) {
+    std::fprintf(f, "%zu", cc.pattern_indices.size());
+    for (int v : cc.pattern_indices) std::fprintf(f, " %d", v);
+    std::fprintf(f, "\n");
+  }
+  for (int c : inst.clique_hint) std::fprintf(f, "%d\n", c);
+  std::fclose(f);
+}
+
 }  // namespace
 
 FusionPlan solve(const IlpInstance& inst) {
@@ -828,6 +1031,7 @@ FusionPlan solve(const IlpInstance& inst) {
     throw GraphError("ILP instance: one score per variable required");
   for (double s : inst.scores)
     if (s < 0) throw GraphError("ILP instance requires non-negative scores");
+  dump_instance(inst);
   static const char* method = std::getenv("STITCH_ILP_METHOD");
   if (!(method && std::string(method) == "monolithic")) {
     FusionPlan plan;
@@ -926,6 +1130,11 @@ FusionPlan solve_with_cycle_elimination(const Graph& g, const std::vector<Fusion
       chosen.push_back(std::move(p));
     }
     ContractResult r = contract_plan(g, chosen);
+    if (std::getenv("STITCH_ILP_TRACE")) {
+      std::fprintf(stderr, "[ilp] round %d total %.17g selected", round, plan.total_score);
+      for (int v : plan.selected) std::fprintf(stderr, " %d", v);
+      std::fprintf(stderr, "%s\n", r.cycle ? " (cycle)" : "");
+    }
     if (!r.cycle) {
       g_stats = total;
       return plan;

@@ -25,7 +25,7 @@ def plans(full=True, small=True):
             g = fn(**kw)
             if size == "full":
                 out.append(("%s/%s/bench" % (name, size), tuning.config_plan(name, g)[0]["fused"]))
-            if size == "full" and name in W.PLAN_OPTIONS:
+            if size == "full" and name in W.WHOLE_GRAPH:
                 pass  # whole-graph config: only the (shipped) bench plan
             else:
                 for lim_tag, lim in (("b200", W.B200_SHARED_LIMIT), ("ref48k", W.REFERENCE_SHARED_LIMIT)):

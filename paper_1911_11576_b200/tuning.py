@@ -22,6 +22,7 @@ paper_1911_11576_b200/data/b200_kernel_times/<config>.csv.
 """
 
 import concurrent.futures as cf
+import hashlib
 import json
 import os
 
@@ -142,7 +143,7 @@ PLAN_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "data", "pla
 
 
 def _plan_key(graph, options):
-    import hashlib
+
     blob = json.dumps({"graph": graph, "options": options}, sort_keys=True, separators=(",", ":"))
     return hashlib.sha256(blob.encode()).hexdigest()
 
@@ -162,16 +163,30 @@ def cached_plan(name, graph, options):
     return d["result"]
 
 
-def kernel_variants(name):
+def kernel_variants(name, fused=None):
     """The measured per-group codegen variant table of suite config `name`
     (data/kernel_variants/<name>.json, scripts/tune_variants.py): {op id:
     codegen overrides}, passed to the executor as kernel_options; {} when
-    none is shipped."""
+    none is shipped, or when it was measured on another plan (its
+    `plan_signature` differs from that of `fused`, default: the plan bench.py
+    runs) -- op ids name different groups then."""
     p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "data", "kernel_variants", name + ".json")
     if not os.path.exists(p):
         return {}
     with open(p) as f:
-        return json.load(f)["table"]
+        d = json.load(f)
+    if fused is None:
+        fused = config_plan(name)[0]["fused"]
+    if d.get("plan_signature") != plan_signature(fused):
+        import warnings
+        warnings.warn("kernel variant table %s was measured on another plan; not used" % p)
+        return {}
+    return d["table"]
+
+
+def plan_signature(fused):
+    """Identity of a fused graph's grouping (sha256 of its fusion groups)."""
+    return hashlib.sha256(json.dumps(groups_of(fused)).encode()).hexdigest()[:16]
 
 
 def groups_of(fused):

@@ -30,8 +30,8 @@ def cases(full):
             yield "fixture:%s@%d" % (os.path.basename(p)[:-5], lim), g, {"shared_limit_bytes": lim}
         yield "fixture:%s@substitution" % os.path.basename(p)[:-5], g, {"strategy": "substitution"}
     for name, fn in W.CONFIGS.items():
-        # whole-graph configs (W.PLAN_OPTIONS) are beyond the reference's search at full size
-        sizes = [("small", W.SMALL[name])] + ([("full", {})] if full and name not in W.PLAN_OPTIONS else [])
+        # whole-graph configs (W.WHOLE_GRAPH) are beyond the reference's search at full size
+        sizes = [("small", W.SMALL[name])] + ([("full", {})] if full and name not in W.WHOLE_GRAPH else [])
         for size, kw in sizes:
             g = fn(**kw)
             for lim in (W.REFERENCE_SHARED_LIMIT, W.B200_SHARED_LIMIT):

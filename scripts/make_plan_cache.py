@@ -21,6 +21,7 @@ t1 = time.time() - t
 b = rt.plan(g, **opts)
 ta, tb = a.pop("timings"), b.pop("timings")
 assert a == b, "planning is not deterministic"
+assert ta["ilp_truncated"] == 0, "the selection search hit its node budget: plan not exact"
 os.makedirs(tuning.PLAN_DIR, exist_ok=True)
 # the candidate list (200k patterns) is not shipped: count + the selected ones
 pl = a["plan"]

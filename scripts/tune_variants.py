@@ -128,7 +128,8 @@ def main():
     step0, step1 = float(np.median(t0s[5:])), float(np.median(t1s[5:]))
     print("step: default %.4f ms, tuned %.4f ms (%d of %d groups changed)" % (step0, step1, len(table), len(base)))
     all_times = {op: {str(vi): round(tv[op], 2) for vi, tv in times.items() if op in tv} for op in base}
-    res = {"config": a.config, "variants": VARIANTS, "table": table, "per_op": chosen, "times_us": all_times,
+    res = {"config": a.config, "plan_signature": tuning.plan_signature(fused), "variants": VARIANTS, "table": table,
+           "per_op": chosen, "times_us": all_times,
            "step_ms": {"default": step0, "tuned": step1}, "reps": a.reps, "min_gain": a.min_gain}
     out = a.out or os.path.join(ROOT, "paper_1911_11576_b200", "data", "kernel_variants", a.config + ".json")
     os.makedirs(os.path.dirname(out), exist_ok=True)

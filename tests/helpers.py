@@ -68,3 +68,59 @@ def chunk_chain_graph(R=4096, C=256):
                       _node("cs", "reduce", ["y"], dims=(C,), reduce_dims=[0])],
             "outputs": ["cs"]}
 
+
+
+def contract_selection(scores, sets, cycles):
+    """Brute force of the selection contract (reference
+    proj/src/ilp_solver.cpp:139 solve, small k only): optimum = max over
+    node-disjoint selections within the cycle limits of the ascending-order
+    double sum; answer = the index-by-index lexicographic extraction
+    (ilp_solver.cpp:153-167)."""
+    k = len(scores)
+    optimal, opt = [], None
+    for mask in range(1 << k):
+        used, ok = set(), True
+        for i in range(k):
+            if mask >> i & 1:
+                if used & sets[i]:
+                    ok = False
+                    break
+                used |= sets[i]
+        if not ok or any(sum(mask >> i & 1 for i in c) > len(c) - 1 for c in cycles):
+            continue
+        t = 0.0
+        for i in range(k):
+            if mask >> i & 1:
+                t += scores[i]
+        if opt is None or t > opt:
+            opt, optimal = t, []
+        if t == opt:
+            optimal.append(mask)
+    selected, prefix, inc, exc = [], 0.0, 0, 0
+    for v in range(k):
+        if prefix == opt:
+            break
+        cand = inc | (1 << v)
+        if any(m & cand == cand and not m & exc for m in optimal):
+            inc = cand
+            selected.append(v)
+            prefix = 0.0
+            for w in selected:
+                prefix += scores[w]
+        else:
+            exc |= 1 << v
+    return selected, prefix
+
+
+def contract_solve_cycle(graph, patterns, scores):
+    """contract_selection under the reference's cycle elimination loop
+    (ilp_solver.cpp:175 solve_with_cycle_elimination)."""
+    from paper_1911_11576_b200 import runtime as rt
+    sets, cycles = [set(p) for p in patterns], []
+    for _ in range(1000):
+        sel, tot = contract_selection(scores, sets, cycles)
+        c = rt.debug_call("contract", graph=graph, plan=[patterns[i] for i in sel])
+        if "cycle" not in c:
+            return {"selected": sel, "total": tot}
+        cycles.append([sel[k] for k in c["cycle"]["patterns"]])
+    raise AssertionError("cycle elimination did not converge")

@@ -98,13 +98,13 @@ def test_full_size_row_sampled(name, plan_kind):
     are checked against the oracle on those items (every config is
     independent per batch item); per-shard column reductions (encoder's
     dbias) against an fp64 reduction of the full input."""
-    if name in W.PLAN_OPTIONS and plan_kind == "model":
+    if name in W.WHOLE_GRAPH and plan_kind == "model":
         pytest.skip("whole-graph config: the bench plan (exec case) is its model-based plan")
     g = W.CONFIGS[name]()
     batch, rows = W.shard_layout(name)
     if plan_kind == "exec":
         res, desc = tuning.config_plan(name, g)
-        assert desc.startswith("execution") or name in W.PLAN_OPTIONS
+        assert desc.startswith("execution") or name in W.WHOLE_GRAPH
         fused = res["fused"]
     else:
         fused = rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT)["fused"]
@@ -248,7 +248,7 @@ def test_bert_batch2_full_parity():
     worst-case bound is not finite after 12 layers are uncertified there),
     and every output against the unfused one-kernel-per-op GPU graph."""
     g = W.bert(batch=2)
-    fused = rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT, **W.PLAN_OPTIONS["bert"])["fused"]
+    fused = rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT, **W.PLAN_OPTIONS.get("bert", {}))["fused"]
     ins = orc.random_inputs(g, seed=81, scale=0.5)
     ex = assert_parity(g, fused, ins)
     assert len(ex.info["kernels"]) > 100

@@ -17,7 +17,7 @@ import random
 import pytest
 
 from conftest import strip_plan
-from helpers import random_dag
+from helpers import contract_solve_cycle, random_dag
 from paper_1911_11576_b200 import runtime as rt
 from paper_1911_11576_b200 import workloads as W
 
@@ -132,6 +132,54 @@ def test_cycle_elimination_random(ref, seed):
     assert a == b
     chosen = [pats[i] for i in a["selected"]]
     assert "cycle" not in rt.debug_call("contract", graph=g, plan=chosen)
+
+
+@pytest.mark.parametrize("seed", range(80))
+def test_cycle_elimination_degenerate(ref, seed):
+    """Tie-heavy selection instances (the shape of the whole-graph BERT
+    instance): pattern scores are sums of per-op weights, so every way of
+    covering the same ops is a tie in real arithmetic and the LP relaxation
+    has many zero-reduced-cost columns; only the ascending-order double sums
+    separate the ties. Exercises the rounding window, reduced-cost fixing
+    and the split into independent pieces against the reference's
+    exhaustive search and lexicographic extraction."""
+    rng = random.Random(5000 + seed)
+    g = random_dag(seed, n_ops=8 + seed % 7)
+    ids = [n["id"] for n in g["nodes"] if n["kind"] != "parameter"]
+    w = {i: rng.choice([0.1, 0.2, 0.3, 0.7, 1.1, 1e-3, 3.3]) * rng.choice([1, 10, 1e4]) for i in ids}
+    pats = []
+    for _ in range(rng.randint(4, 14)):
+        p = sorted(rng.sample(ids, rng.randint(1, min(4, len(ids)))))
+        if p not in pats:
+            pats.append(p)
+    scores = []
+    for p in pats:
+        t = 0.0
+        for i in (p if rng.random() < 0.5 else reversed(p)):
+            t += w[i]
+        scores.append(t if rng.random() < 0.9 else 0.0)
+    a, b = both(ref, "solve_cycle", graph=g, patterns=pats, scores=scores)
+    want = contract_solve_cycle(g, pats, scores)
+    assert a == want
+    if seed in REFERENCE_ROUNDING_DEFECTS:
+        # the reference's own search misses its optimum here (below)
+        assert b != want and b["total"] < want["total"]
+    else:
+        assert a == b
+    chosen = [pats[i] for i in a["selected"]]
+    assert "cycle" not in rt.debug_call("contract", graph=g, plan=chosen)
+
+
+# Instances of test_cycle_elimination_degenerate where the reference violates
+# its own contract: ValueSearch::descend (ilp_solver.cpp:127) prunes with
+# canonical_total() + remaining <= best_, `remaining` being a running double
+# difference; on near-tie instances its rounding lands the bound just under
+# the canonical optimum, a fixed-prefix probe of the extraction
+# (ilp_solver.cpp:160) then never reproduces `optimum` exactly, and the
+# reference returns a non-optimal selection (seed 39: the empty one, total
+# 0.0, where 11.2 is feasible). This solver follows the contract there
+# (brute force: tests/helpers.py contract_selection); 1 of 200 seeds checked.
+REFERENCE_ROUNDING_DEFECTS = {39}
 
 
 @pytest.mark.parametrize("seed", range(20))
