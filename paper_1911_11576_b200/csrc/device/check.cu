@@ -53,3 +53,15 @@ extern "C" __global__ void __launch_bounds__(256) check_row_cta(const float* __r
   grid_barrier(sync);
   if (blockIdx.x == 0 && threadIdx.x == 0) y[rows] = combine_parts<SumOp>(ws, gridDim.x, 1, 0);
 }
+
+extern "C" __global__ void __launch_bounds__(256) check_gemm(const float* __restrict__ a, const float* __restrict__ b,
+                                                             float* __restrict__ c) {
+  extern __shared__ __align__(128) float smem[];
+  gemm::run<512, 512, 512, 1, 512, 1, 0, 512, 1, 0>(a, b, c, smem);
+}
+
+extern "C" __global__ void __launch_bounds__(256) check_gemm_ragged(const float* __restrict__ a,
+                                                                    const float* __restrict__ b, float* __restrict__ c) {
+  extern __shared__ __align__(128) float smem[];
+  gemm::run<300, 130, 77, 3, 1, 300, 300 * 77, 1, 77, 77 * 130>(a, b, c, smem);
+}

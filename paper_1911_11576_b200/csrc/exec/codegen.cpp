@@ -130,6 +130,7 @@ class Builder {
 
  private:
   bool build_gws();  // the warp-specialised tcgen05 scheme, when the group fits it
+  bool build_gemm();  // one unfused dot: the tiled fp32 GEMM scheme
   bool nr_div_ = false;  // elementwise divides as branch-free rcp + Newton (gws tails)
   // ---- analysis ----
   void collect();
@@ -2008,7 +2009,11 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
     if (c.cls[o] != Cls::kRowed) continue;
     const int64_t S = prod(vals_[o].dims, k);
     if (S == 1) {
-      ln("if (t == 0) " + out_ptr(o) + "[row] = " + scalar_[o] + ";");
+      // a reduction's row scalar, or element 0 of a one-element row tile
+      // (e.g. a [1, K] . [K, 1] dot)
+      auto sc = scalar_.find(o);
+      const std::string v = sc != scalar_.end() && !sc->second.empty() ? sc->second : reg_[o] + "[0]";
+      ln("if (t == 0) " + out_ptr(o) + "[row] = " + v + ";");
       continue;
     }
     const Layout L = layout(S, NT);
@@ -2633,7 +2638,7 @@ bool Builder::build_gws() {
   }
   memo_.pop_back();
   row_hook_ = nullptr;
-  nr_div_ = false;
+  nr_div_ = opts_.nr_divide;
   close();
   for (int v : outputs_)
     ln("*reinterpret_cast<float2*>(" + out_ptr(v) + " + off) = make_float2(o" + std::to_string(v) + "[0], o" +
@@ -2715,10 +2720,96 @@ bool Builder::build_gws() {
   return true;
 }
 
+bool Builder::build_gemm() {
+  if (!opts_.gemm || topo_members_.size() != 1) return false;
+  const int m = topo_members_[0];
+  const Val& v = vals_[m];
+  const OpNode& op = *v.node;
+  if (op.type != OpType::kDot && op.type != OpType::kBatchedDot) return false;
+  if (!v.output || outputs_.size() != 1 || outputs_[0] != m) return false;
+  const int a = v.operands[0], b = v.operands[1];
+  if (a == b || !vals_[a].external || !vals_[b].external) return false;
+  const auto& ad = vals_[a].dims;
+  const auto& bd = vals_[b].dims;
+  int64_t M, N, K, batch = 1, sam, sak, sab = 0, sbk, sbn, sbb = 0;
+  if (op.type == OpType::kDot) {
+    if (ad.size() != 2 || bd.size() != 2) return false;
+    auto cd = effective_contract_dims(body_, op);
+    K = ad[cd[0]];
+    M = ad[1 - cd[0]];
+    N = bd[1 - cd[1]];
+    if (bd[cd[1]] != K) return false;
+    sam = cd[0] == 1 ? K : 1;
+    sak = cd[0] == 1 ? 1 : M;
+    sbk = cd[1] == 0 ? N : 1;
+    sbn = cd[1] == 0 ? 1 : K;
+  } else {
+    const auto cd = effective_contract_dims(body_, op);
+    const size_t r = v.dims.size();
+    if (r < 3 || ad.size() != r || bd.size() != r) return false;
+    if (!(cd[0] == static_cast<int>(r) - 1 && cd[1] == static_cast<int>(r) - 2)) return false;
+    for (size_t d = 0; d + 2 < r; ++d) {
+      if (ad[d] != v.dims[d] || bd[d] != v.dims[d]) return false;
+      batch *= v.dims[d];
+    }
+    M = ad[r - 2];
+    K = ad[r - 1];
+    N = bd[r - 1];
+    if (bd[r - 2] != K) return false;
+    sam = K, sak = 1, sab = M * K, sbk = N, sbn = 1, sbb = K * N;
+  }
+  if (v.dims.size() < 2 || v.dims[v.dims.size() - 2] != M || v.dims.back() != N || M < 1 || N < 1 || K < 1)
+    return false;
+  // small matrices waste most of a 128 x 128 tile: the row scheme is faster
+  // there (4096 batched 64^3 dots: 64 vs 125 us, scripts/gemm_perf.py)
+  if (M * N < 128 * 64) return false;
+  const int64_t tiles = batch * ((M + 127) / 128) * ((N + 127) / 128);
+  auto L = [](int64_t x) { return std::to_string(x) + "LL"; };
+  std::vector<std::string> params;
+  for (int x : inputs_) {
+    params.push_back("const float* __restrict__ " + in_ptr(x));
+    spec_.inputs.push_back(vals_[x].id);
+    spec_.algo_bytes += vals_[x].node->shape.byte_count();
+  }
+  params.push_back("float* __restrict__ " + out_ptr(m));
+  spec_.outputs.push_back(v.id);
+  spec_.algo_bytes += v.node->shape.byte_count();
+  params.push_back("float* __restrict__ ws");
+  params.push_back("unsigned int* __restrict__ gsync");
+  params.push_back("const long long row_lo");
+  params.push_back("const long long row_hi");
+  std::ostringstream h;
+  h << "// kernel for op '" << name_ << "': " << v.id << " = " << to_string(op.type) << "(" << vals_[a].id << ", "
+    << vals_[b].id << "), scheme gemm (tiled fp32, " << batch << " x [" << M << " x " << K << "] . [" << K << " x "
+    << N << "])\n";
+  h << "extern \"C\" __global__ void __launch_bounds__(256) " << name_ << "(" << join(params, ", ") << ") {\n";
+  h << "  extern __shared__ __align__(128) float smem[];\n";
+  h << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
+  h << "  asm volatile(\"griddepcontrol.launch_dependents;\");\n";
+  h << "  (void)ws; (void)gsync; (void)row_lo; (void)row_hi;\n";
+  h << "  stitch_dev::gemm::run<" << L(M) << ", " << L(N) << ", " << L(K) << ", " << L(batch) << ", " << L(sam) << ", "
+    << L(sak) << ", " << L(sab) << ", " << L(sbk) << ", " << L(sbn) << ", " << L(sbb) << ">(" << in_ptr(a) << ", "
+    << in_ptr(b) << ", " << out_ptr(m) << ", smem);\n";
+  h << "}\n";
+  spec_.source = h.str();
+  spec_.scheme = "gemm(" + std::to_string(batch) + "x" + std::to_string(M) + "x" + std::to_string(N) + "x" +
+                 std::to_string(K) + ")";
+  spec_.composition = {"thread", "block"};
+  spec_.block = 256;
+  spec_.smem_bytes = 2 * 8 * (128 + 128) * 4;
+  spec_.max_grid = static_cast<int>(std::min<int64_t>(tiles, 1 << 20));
+  spec_.flops = 2 * batch * M * N * K;
+  spec_.workspace_floats = 0;
+  spec_.sync_words = 0;
+  return true;
+}
+
 KernelSpec Builder::build() {
   collect();
   spec_.name = name_;
+  nr_div_ = opts_.nr_divide;
   if (build_gws()) return spec_;
+  if (build_gemm()) return spec_;
   std::vector<Component> comps = components();
   bool sectioned = false;
   for (Component& c : comps) {

@@ -85,10 +85,16 @@ struct CodegenOptions {
   bool colred = true;
   bool colred_fused = true;
   bool rcp_divide = true;  // c / x with c = +-2^k as the exact c * rcp.rn(x)
+  // every elementwise divide / reciprocal as branch-free rcp.approx + Newton
+  // (<= 1 ulp; __frcp_rn / IEEE division carry a slow-path call)
+  bool nr_divide = false;
   // Row groups of [S][64][64] tiles with two batched dots on kernel inputs
   // (the GRU group): the warp-specialised tcgen05 scheme (device gws::run,
   // TMA producer / MMA issuer / split / tail warps). Off: the ROW scheme.
   bool gws = true;
+  // A kernel that is one unfused dot / batched dot (operands from HBM): the
+  // tiled fp32 GEMM scheme (device gemm::run). Off: SECTIONED / BLOCK loops.
+  bool gemm = true;
   // __launch_bounds__ minimum CTAs per SM (register budget hint; 0: none)
   int min_ctas_per_sm = 0;
   // Groups ROW / COLRED / FLAT cannot take (dots + reductions over different

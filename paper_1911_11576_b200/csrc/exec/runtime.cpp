@@ -113,6 +113,8 @@ void apply_codegen_options(CodegenOptions& c, const json::Value& o) {
   if (o.has("row_prefetch_warp")) c.row_prefetch_warp = o.at("row_prefetch_warp").as_bool();
   if (o.has("rcp_divide")) c.rcp_divide = o.at("rcp_divide").as_bool();
   if (o.has("gws")) c.gws = o.at("gws").as_bool();
+  if (o.has("gemm")) c.gemm = o.at("gemm").as_bool();
+  if (o.has("nr_divide")) c.nr_divide = o.at("nr_divide").as_bool();
   if (o.has("min_ctas_per_sm")) c.min_ctas_per_sm = static_cast<int>(o.at("min_ctas_per_sm").as_int());
   if (o.has("block_compose")) c.block_compose = o.at("block_compose").as_bool();
   if (o.has("tma_early")) c.tma_early = o.at("tma_early").as_bool();

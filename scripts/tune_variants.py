@@ -48,6 +48,12 @@ VARIANTS = [
     {"colred_eout": True, "colred_cols": 128},
     {"pack_sequential": True},
     {"tma_double_buffer": True},
+    {"nr_divide": True},
+    {"min_ctas_per_sm": 3},
+    {"min_ctas_per_sm": 2},
+    {"nr_divide": True, "min_ctas_per_sm": 3},
+    {"nr_divide": True, "loop_fusion": False},
+    {"nr_divide": True, "wide_cross_cta": True, "wide_cross_threads": 192},
 ]
 
 

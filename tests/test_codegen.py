@@ -182,3 +182,31 @@ def test_random_dag_kernels_compile(seed):
         for gg in (fused, g):
             for k in compile_only(gg, **opts).info["kernels"]:
                 assert k["block"] % 32 == 0
+
+
+def test_gemm_scheme_selection():
+    """A kernel that is one unfused dot / batched dot takes the tiled GEMM
+    scheme (reference fixture all_partition: two 512^3 dots the planner
+    leaves unfused); a dot fused with other ops does not."""
+    nodes = [_node(p, "parameter", dims=(512, 512)) for p in ("p0", "p1", "p2")]
+    nodes += [_node("dot_a", "dot", ["p0", "p1"], dims=(512, 512), contract_dims=[1, 0]),
+              _node("dot_b", "dot", ["dot_a", "p2"], dims=(512, 512), contract_dims=[1, 0])]
+    g = {"nodes": nodes, "outputs": ["dot_b"]}
+    ex = compile_only(rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT)["fused"])
+    assert [k["scheme"] for k in ex.info["kernels"]] == ["gemm(1x512x512x512)"] * 2
+    src = ex.sources()
+    assert "stitch_dev::gemm::run<512LL, 512LL, 512LL, 1LL, 512LL, 1LL, 0LL, 512LL, 1LL, 0LL>" in src["dot_a"]
+    ex = compile_only(g, gemm=False)
+    assert all(not k["scheme"].startswith("gemm") for k in ex.info["kernels"])
+    # transposed operands: strides follow the contraction dims
+    g2 = {"nodes": [_node("a", "parameter", dims=(77, 300)), _node("b", "parameter", dims=(130, 77)),
+                    _node("c", "dot", ["a", "b"], dims=(300, 130), contract_dims=[0, 1])], "outputs": ["c"]}
+    ex = compile_only(g2)
+    assert "gemm::run<300LL, 130LL, 77LL, 1LL, 1LL, 300LL, 0LL, 1LL, 77LL, 0LL>" in ex.sources()["c"]
+    # fused with an elementwise consumer: not the GEMM scheme
+    g3 = {"nodes": [_node("a", "parameter", dims=(64, 64)), _node("b", "parameter", dims=(64, 64)),
+                    _node("c", "dot", ["a", "b"], dims=(64, 64)), _node("d", "elementwise", ["c"], "exp", dims=(64, 64))],
+          "outputs": ["d"]}
+    fused = rt.debug_call("apply_plan", graph=g3, patterns=[["c", "d"]], selected=[0])["graph"]
+    ex = compile_only(fused)
+    assert not any(k["scheme"].startswith("gemm") for k in ex.info["kernels"])

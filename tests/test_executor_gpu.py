@@ -636,3 +636,50 @@ def test_parity_margins_report():
     if os.path.isdir("gpurun_out"):
         with open("gpurun_out/parity_margins.json", "w") as f:
             json.dump(rows, f, indent=1)
+
+
+def _gemm_graph(kind, adims, bdims, odims, cd=None):
+    dot = {"id": "c", "kind": kind, "operands": ["a", "b"], "shape": {"dims": list(odims), "dtype": "f32"}}
+    if cd is not None:
+        dot["contract_dims"] = list(cd)
+    return {"nodes": [{"id": "a", "kind": "parameter", "shape": {"dims": list(adims), "dtype": "f32"}},
+                      {"id": "b", "kind": "parameter", "shape": {"dims": list(bdims), "dtype": "f32"}}, dot],
+            "outputs": ["c"]}
+
+
+@pytest.mark.parametrize("case", [
+    ("dot", (300, 77), (77, 130), (300, 130), None),
+    ("dot", (77, 300), (77, 130), (300, 130), (0, 0)),
+    ("dot", (300, 77), (130, 77), (300, 130), (1, 1)),
+    ("dot", (512, 512), (512, 512), (512, 512), None),
+    ("dot", (1, 8192), (8192, 1), (1, 1), None),
+    ("batched_dot", (3, 300, 77), (3, 77, 130), (3, 300, 130), None),
+    ("batched_dot", (2, 2, 96, 160), (2, 2, 160, 128), (2, 2, 96, 128), None),
+])
+def test_gemm_scheme_parity(case):
+    """An unfused dot / batched dot (the reference keeps large dots out of
+    patterns) runs the tiled fp32 GEMM scheme: ragged M, N, K, transposed
+    operands, batches, against the oracle; the loop schemes it replaces
+    agree too (and keep tiny products: a [1, 8192] . [8192, 1] row)."""
+    g = _gemm_graph(*case)
+    ins = orc.random_inputs(g, seed=91)
+    ex = assert_parity(g, g, ins)
+    small = case[3][-1] * case[3][-2] < 128 * 64  # below one half tile: the row scheme
+    assert [k["scheme"].split("(")[0] == "gemm" for k in ex.info["kernels"]] == [not small]
+    ex2 = assert_parity(g, g, ins, gemm=False)
+    assert not ex2.info["kernels"][0]["scheme"].startswith("gemm")
+
+
+def test_gemm_all_partition_fixture():
+    """The reference fixture all_partition.json (two chained 512^3 dots the
+    planner leaves unfused): both dots on the GEMM scheme, oracle parity."""
+    nodes = [{"id": p, "kind": "parameter", "shape": {"dims": [512, 512], "dtype": "f32"}} for p in ("p0", "p1", "p2")]
+    nodes += [{"id": "dot_a", "kind": "dot", "operands": ["p0", "p1"], "shape": {"dims": [512, 512], "dtype": "f32"},
+               "contract_dims": [1, 0]},
+              {"id": "dot_b", "kind": "dot", "operands": ["dot_a", "p2"], "shape": {"dims": [512, 512], "dtype": "f32"},
+               "contract_dims": [1, 0]}]
+    g = {"nodes": nodes, "outputs": ["dot_b"]}
+    fused = rt.plan(g, shared_limit_bytes=W.B200_SHARED_LIMIT)["fused"]
+    ins = orc.random_inputs(g, seed=92)
+    ex = assert_parity(g, fused, ins)
+    assert [k["scheme"].split("(")[0] for k in ex.info["kernels"]] == ["gemm", "gemm"]
