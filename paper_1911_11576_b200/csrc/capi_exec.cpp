@@ -59,6 +59,7 @@ int stitch_executor_create(const char* fused_graph_json, const char* options_jso
     if (o.has("chunking")) opts.chunking = o.at("chunking").as_bool();
     if (o.has("chunk_l2_bytes")) opts.chunk_l2_bytes = o.at("chunk_l2_bytes").as_int();
     if (o.has("pdl")) opts.pdl = o.at("pdl").as_bool();
+    if (o.has("concurrent_lanes")) opts.concurrent_lanes = static_cast<int>(o.at("concurrent_lanes").as_int());
     if (o.has("fold_constants")) opts.fold_constants = o.at("fold_constants").as_bool();
     if (o.has("sink_broadcasts")) opts.sink_broadcasts = o.at("sink_broadcasts").as_bool();
     if (o.has("overlap_copies")) opts.overlap_copies = o.at("overlap_copies").as_bool();

@@ -152,6 +152,7 @@ Executor::Executor(const Graph& fused, const ExecOptions& opts) : g_(fused), opt
   }
   build_kernels();
   plan_chunks();
+  plan_deps();
   plan_arena();
   if (!opts_.compile_only) init_device();
 }
@@ -169,6 +170,8 @@ Executor::~Executor() {
     if (st) cu.cuStreamDestroy(static_cast<CUstream>(st));
   for (void* e : lane_events_) cu.cuEventDestroy(static_cast<CUevent>(e));
   for (void* st : lanes_) cu.cuStreamDestroy(static_cast<CUstream>(st));
+  for (void* e : dag_events_) cu.cuEventDestroy(static_cast<CUevent>(e));
+  for (void* st : dag_lanes_) cu.cuStreamDestroy(static_cast<CUstream>(st));
   for (KernelInst& k : kernels_)
     if (k.module) cu.cuModuleUnload(static_cast<CUmodule>(k.module));
   if (arena_) cu.cuMemFree(arena_);
@@ -480,7 +483,8 @@ void Executor::plan_arena() {
     std::vector<std::pair<int64_t, int64_t>> busy;
     for (int p : placed) {
       const ValueBuf& y = bufs_[p];
-      if (y.first <= x.last && x.first <= y.last) busy.push_back({y.offset, y.offset + y.arena_bytes()});
+      const bool live = dag_ ? !(ordered_before(b, p) || ordered_before(p, b)) : (y.first <= x.last && x.first <= y.last);
+      if (live) busy.push_back({y.offset, y.offset + y.arena_bytes()});
     }
     std::sort(busy.begin(), busy.end());
     int64_t off = 0;
@@ -493,11 +497,91 @@ void Executor::plan_arena() {
     placed.push_back(b);
   }
   for (KernelInst& k : kernels_) {
-    k.ws_off = 0;
+    k.ws_off = 0;  // serial schedule: one shared workspace
     ws_floats_ = std::max(ws_floats_, k.spec.workspace_floats);
     k.sync_off = sync_words_;
     sync_words_ += std::max(2, k.spec.sync_words) + 30;  // one 128-byte line per kernel
   }
+  if (!dag_) return;
+  // Workspace: kernels that may run concurrently (neither an ancestor of the
+  // other) get disjoint ranges; an ancestor's range is free again.
+  const int nk = static_cast<int>(kernels_.size());
+  ws_floats_ = 0;
+  for (int k = 0; k < nk; ++k) {
+    const int64_t need = (kernels_[k].spec.workspace_floats + 63) / 64 * 64;
+    std::vector<std::pair<int64_t, int64_t>> busy;
+    for (int j = 0; j < k; ++j)
+      if (!(anc_[k][j / 64] >> (j % 64) & 1) && kernels_[j].spec.workspace_floats > 0)
+        busy.push_back({kernels_[j].ws_off, kernels_[j].ws_off + kernels_[j].spec.workspace_floats});
+    std::sort(busy.begin(), busy.end());
+    int64_t off = 0;
+    for (auto [lo, hi] : busy) {
+      if (off + need <= lo) break;
+      off = std::max(off, (hi + 63) / 64 * 64);
+    }
+    kernels_[k].ws_off = need > 0 ? off : 0;
+    ws_floats_ = std::max(ws_floats_, off + need);
+  }
+  // invariant: values sharing arena bytes are ordered by true dependencies
+  for (size_t a = 0; a < bufs_.size(); ++a)
+    for (size_t b = a + 1; b < bufs_.size(); ++b) {
+      const ValueBuf &x = bufs_[a], &y = bufs_[b];
+      if (x.kind != ValueBuf::kArena || y.kind != ValueBuf::kArena) continue;
+      if (x.offset >= y.offset + y.arena_bytes() || y.offset >= x.offset + x.arena_bytes()) continue;
+      if (!ordered_before(static_cast<int>(a), static_cast<int>(b)) && !ordered_before(static_cast<int>(b), static_cast<int>(a)))
+        throw InternalError("dataflow arena: " + x.key + " and " + y.key + " share memory but may run concurrently");
+    }
+}
+
+void Executor::plan_deps() {
+  // Dataflow launch order (ExecOptions::concurrent_lanes): true dependencies
+  // only. Arena placement (plan_arena) then lets two values share memory
+  // only when every kernel touching one is an ancestor of the other's
+  // producer, so memory reuse adds no edge.
+  const int nk = static_cast<int>(kernels_.size());
+  dag_ = opts_.concurrent_lanes > 1 && nk > 1;
+  for (const Segment& sg : segments_) dag_ = dag_ && sg.chunks == 1;
+  preds_.assign(nk, {});
+  writer_.assign(bufs_.size(), -1);
+  touch_.assign(bufs_.size(), {});
+  for (int k = 0; k < nk; ++k) {
+    for (int b : kernels_[k].out_bufs) {
+      writer_[b] = k;
+      touch_[b].push_back(k);
+    }
+    for (int b : kernels_[k].in_bufs) touch_[b].push_back(k);
+  }
+  if (!dag_) return;
+  int last_coop = -1;
+  for (int k = 0; k < nk; ++k) {
+    std::set<int> p;
+    for (int b : kernels_[k].in_bufs)  // read after write
+      if (writer_[b] >= 0 && writer_[b] != k) p.insert(writer_[b]);
+    // grid-barrier kernels spin until every CTA is resident: never two in
+    // flight (every other kernel in flight runs to completion unconditionally,
+    // and PDL dependents launch only once all of their primary's CTAs run)
+    if (kernels_[k].spec.cooperative) {
+      if (last_coop >= 0) p.insert(last_coop);
+      last_coop = k;
+    }
+    preds_[k].assign(p.begin(), p.end());
+  }
+  const size_t words = (static_cast<size_t>(nk) + 63) / 64;
+  anc_.assign(nk, std::vector<uint64_t>(words, 0));
+  for (int k = 0; k < nk; ++k)
+    for (int q : preds_[k]) {
+      for (size_t w = 0; w < words; ++w) anc_[k][w] |= anc_[q][w];
+      anc_[k][q / 64] |= 1ull << (q % 64);
+    }
+}
+
+bool Executor::ordered_before(int a, int b) const {
+  // every kernel touching value a finishes before value b's producer starts
+  const int w = writer_[b];
+  if (w < 0) return false;
+  for (int t : touch_[a])
+    if (!(anc_[w][t / 64] >> (t % 64) & 1)) return false;
+  return true;
 }
 
 void Executor::init_device() {
@@ -596,6 +680,18 @@ void Executor::init_device() {
     cu_check(cu.cuEventCreate(&x, CU_EVENT_DISABLE_TIMING), "lane event");
     lane_events_.push_back(x);
   }
+  if (dag_) {
+    for (int j = 1; j < opts_.concurrent_lanes; ++j) {
+      CUstream st;
+      cu_check(cu.cuStreamCreate(&st, CU_STREAM_NON_BLOCKING), "dag lane stream");
+      dag_lanes_.push_back(st);
+    }
+    for (size_t e = 0; e <= kernels_.size(); ++e) {
+      CUevent x;
+      cu_check(cu.cuEventCreate(&x, CU_EVENT_DISABLE_TIMING), "dag event");
+      dag_events_.push_back(x);
+    }
+  }
   device_ready_ = true;
 }
 
@@ -692,9 +788,60 @@ void Executor::launch_one(int i, int c, int chunks, const void* const* inputs, v
   cu_check(cu.cuLaunchKernelEx(&cfg, static_cast<CUfunction>(k.fn), args.data(), nullptr), k.spec.name.c_str());
 }
 
+void Executor::launch_dag(const void* const* inputs, void* const* outputs, void* stream) {
+  // Kernels in launch (topological) order; each goes on the lane whose last
+  // kernel is its latest predecessor, else on a fresh lane, else on the lane
+  // idle longest, and waits on the done-events of its other predecessors'
+  // lanes (only the latest predecessor per lane).
+  CudaApi& cu = CudaApi::get();
+  const int nk = static_cast<int>(kernels_.size());
+  const int nl = static_cast<int>(dag_lanes_.size()) + 1;
+  auto lane_stream = [&](int l) { return static_cast<CUstream>(l == 0 ? stream : dag_lanes_[l - 1]); };
+  auto ev = [&](int k) { return static_cast<CUevent>(dag_events_[k]); };
+  CUevent fork = static_cast<CUevent>(dag_events_[nk]);
+  cu_check(cu.cuEventRecord(fork, lane_stream(0)), "dag fork");
+  std::vector<int> tail(nl, -1), lane_of(nk, -1);
+  std::vector<bool> used(nl, false);
+  used[0] = true;
+  for (int k = 0; k < nk; ++k) {
+    const std::vector<int>& pk = preds_[k];
+    int lane = -1;
+    for (int l = 0; l < nl && lane < 0; ++l)
+      if (!pk.empty() && tail[l] == pk.back()) lane = l;
+    if (lane < 0 && tail[0] < 0) lane = 0;
+    for (int l = 1; l < nl && lane < 0; ++l)
+      if (!used[l]) lane = l;
+    if (lane < 0) {
+      lane = 0;
+      for (int l = 1; l < nl; ++l)
+        if (tail[l] < tail[lane]) lane = l;
+    }
+    CUstream st = lane_stream(lane);
+    if (!used[lane]) {
+      cu_check(cu.cuStreamWaitEvent(st, fork, 0), "dag fork wait");
+      used[lane] = true;
+    }
+    std::vector<int> latest(nl, -1);
+    for (int p : pk) latest[lane_of[p]] = std::max(latest[lane_of[p]], p);
+    for (int l = 0; l < nl; ++l)
+      if (l != lane && latest[l] >= 0) cu_check(cu.cuStreamWaitEvent(st, ev(latest[l]), 0), "dag wait");
+    launch_one(k, 0, 1, inputs, outputs, st);
+    cu_check(cu.cuEventRecord(ev(k), st), "dag done");
+    tail[lane] = k;
+    lane_of[k] = lane;
+  }
+  for (int l = 1; l < nl; ++l)
+    if (used[l] && tail[l] >= 0) cu_check(cu.cuStreamWaitEvent(lane_stream(0), ev(tail[l]), 0), "dag join");
+}
+
 void Executor::launch_all(const void* const* inputs, void* const* outputs, void* stream, std::vector<void*>* events) {
   CudaApi& cu = CudaApi::get();
   CUstream s0 = static_cast<CUstream>(stream);
+  if (dag_ && !events) {
+    launch_dag(inputs, outputs, stream);
+    copy_aliased_outputs(inputs, outputs, stream);
+    return;
+  }
   int launch = 0;
   size_t ev = 0;  // next lane event
   auto next_event = [&]() { return static_cast<CUevent>(lane_events_.at(ev++)); };
@@ -732,6 +879,12 @@ void Executor::launch_all(const void* const* inputs, void* const* outputs, void*
     // Join: s0 continues after every lane's last chunk.
     for (int j = 0; j < m; ++j) cu_check(cu.cuStreamWaitEvent(s0, done[j * sg.chunks + sg.chunks - 1], 0), "join");
   }
+  copy_aliased_outputs(inputs, outputs, stream);
+}
+
+void Executor::copy_aliased_outputs(const void* const* inputs, void* const* outputs, void* stream) {
+  CudaApi& cu = CudaApi::get();
+  CUstream s0 = static_cast<CUstream>(stream);
   for (auto [slot, b] : output_copies_) {
     const ValueBuf& x = bufs_[b];
     CUdeviceptr src = x.kind == ValueBuf::kInput ? reinterpret_cast<CUdeviceptr>(inputs[x.slot])
@@ -1000,6 +1153,11 @@ json::Value Executor::describe() const {
   }
   j.set("schedule", sched);
   j.set("launches", launches_per_run_);
+  int64_t edges = 0;
+  for (const std::vector<int>& p : preds_) edges += static_cast<int64_t>(p.size());
+  j.set("launch_order", dag_ ? "dataflow" : "serial");
+  j.set("concurrent_lanes", dag_ ? opts_.concurrent_lanes : 1);
+  j.set("dependency_edges", edges);
   j.set("folded_constant_kernels", folded_kernels_);
   j.set("sunk_broadcast_kernels", sunk_kernels_);
   j.set("algo_bytes", algo);

@@ -53,6 +53,13 @@ struct ExecOptions {
   int64_t sink_max_bytes = 1 << 20;
   // programmatic dependent launch between consecutive (non-cooperative) kernels
   bool pdl = true;
+  // Dataflow launch: kernels go out on up to `concurrent_lanes` streams
+  // with event edges for their true dependencies only (producer -> consumer,
+  // arena reuse, grid-barrier kernels one at a time), so independent fusion
+  // groups (parameter-gradient column reductions beside the activation-
+  // gradient chain) fill each other's tails. <= 1: one stream in launch order.
+  // Not used for chunked schedules or per-kernel profiling.
+  int concurrent_lanes = 8;
   int chunk_ring = 2;
   CodegenOptions codegen;
   // per fused-op codegen overrides {op id: {option: value}} (the measured
@@ -129,7 +136,11 @@ class Executor {
   void plan_arena();
   void init_device();
   void plan_chunks();
+  void plan_deps();
+  bool ordered_before(int a, int b) const;
   void launch_all(const void* const* inputs, void* const* outputs, void* stream, std::vector<void*>* events);
+  void launch_dag(const void* const* inputs, void* const* outputs, void* stream);
+  void copy_aliased_outputs(const void* const* inputs, void* const* outputs, void* stream);
   void launch_one(int i, int c, int chunks, const void* const* inputs, void* const* outputs, void* stream);
 
   Graph g_;
@@ -143,6 +154,14 @@ class Executor {
   int sunk_kernels_ = 0;
   std::vector<void*> lanes_;        // CUstreams for pipelined chunk lanes
   std::vector<void*> lane_events_;  // CUevents: [segment-local kernel j][chunk c] done, plus fork/join
+  // dataflow launch (ExecOptions::concurrent_lanes)
+  bool dag_ = false;
+  std::vector<std::vector<int>> preds_;  // kernel -> kernels it must follow
+  std::vector<std::vector<uint64_t>> anc_;  // kernel -> ancestor bitset
+  std::vector<int> writer_;                 // value buffer -> producing kernel
+  std::vector<std::vector<int>> touch_;     // value buffer -> kernels reading / writing it
+  std::vector<void*> dag_lanes_;         // CUstreams for lanes 1.. (lane 0 = the caller's stream)
+  std::vector<void*> dag_events_;        // per kernel "done", plus the fork event
   void* copy_streams_[2] = {nullptr, nullptr};  // run_host: H2D and D2H copy streams
   std::vector<void*> in_events_, kernel_events_;
   void* start_event_ = nullptr;
