@@ -79,6 +79,13 @@ STITCH_API int stitch_executor_run_host(stitch_executor* ex, const void* const* 
 STITCH_API int stitch_executor_profile(stitch_executor* ex, const void* const* inputs, void* const* outputs, void* stream,
                             int iters, char** json);
 
+/* Timeline of one pass (executor created with {"trace": true}): runs once
+ * through the normal launch path (CUDA graph, dataflow lanes) and returns
+ * {"kernels":[{"name","start_us","end_us"}...],"span_us":...} from
+ * %globaltimer stamps taken by every warp at kernel entry and exit. */
+STITCH_API int stitch_executor_trace(stitch_executor* ex, const void* const* inputs, void* const* outputs, void* stream,
+                          char** json);
+
 /* Generated CUDA source of every kernel, {"<kernel name>": "<source>"}
  * (the inspectable counterpart of the reference's emitted <fused_op>.cu
  * files, pipeline.cpp:99 / stitch_main.cpp cmd_codegen). */

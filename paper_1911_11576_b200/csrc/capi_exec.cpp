@@ -59,7 +59,9 @@ int stitch_executor_create(const char* fused_graph_json, const char* options_jso
     if (o.has("chunking")) opts.chunking = o.at("chunking").as_bool();
     if (o.has("chunk_l2_bytes")) opts.chunk_l2_bytes = o.at("chunk_l2_bytes").as_int();
     if (o.has("pdl")) opts.pdl = o.at("pdl").as_bool();
+    if (o.has("pdl_cooperative")) opts.pdl_cooperative = o.at("pdl_cooperative").as_bool();
     if (o.has("concurrent_lanes")) opts.concurrent_lanes = static_cast<int>(o.at("concurrent_lanes").as_int());
+    if (o.has("critical_priority")) opts.critical_priority = o.at("critical_priority").as_bool();
     if (o.has("fold_constants")) opts.fold_constants = o.at("fold_constants").as_bool();
     if (o.has("sink_broadcasts")) opts.sink_broadcasts = o.at("sink_broadcasts").as_bool();
     if (o.has("overlap_copies")) opts.overlap_copies = o.at("overlap_copies").as_bool();
@@ -87,6 +89,12 @@ int stitch_executor_run(stitch_executor* ex, const void* const* inputs, void* co
 int stitch_executor_run_host(stitch_executor* ex, const void* const* host_inputs, void* const* host_outputs,
                              void* stream) {
   return guarded([&] { ex->impl->run_host(host_inputs, host_outputs, stream); });
+}
+
+int stitch_executor_trace(stitch_executor* ex, const void* const* inputs, void* const* outputs, void* stream,
+                          char** json_out) {
+  *json_out = nullptr;
+  return guarded([&] { *json_out = dup(ex->impl->trace(inputs, outputs, stream).dump()); });
 }
 
 int stitch_executor_profile(stitch_executor* ex, const void* const* inputs, void* const* outputs, void* stream,

@@ -839,6 +839,12 @@ bool Builder::plan_row(Component& c) {
     c.NT = nt;
   } else {
     c.NT = 32;
+    if (opts_.narrow_rows && c.cross.empty() && c.post.empty() && c.free_out.empty() && max_inner <= opts_.narrow_row_max) {
+      // ~16 elements per lane, 4..32 lanes per row
+      int nt = 4;
+      while (nt < 32 && static_cast<int64_t>(nt) * 16 < max_inner) nt *= 2;
+      c.NT = nt;
+    }
   }
   if (max_inner > static_cast<int64_t>(c.NT) * 64) return false;  // too large for registers
   // shared-memory slab per row group
@@ -1305,8 +1311,8 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
     }
     ln("const long long g0 = blockIdx.x - " + lo + ", gstride = " + n + ";");
   } else {
-    ln("const int t = threadIdx.x & 31;");
-    ln("const int wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;");
+    ln("const int t = threadIdx.x & " + std::to_string(NT - 1) + ";");
+    ln("const int wib = threadIdx.x / " + std::to_string(NT) + ", wpb = blockDim.x / " + std::to_string(NT) + ";");
     ln("float* slab = smem + wib * " + std::to_string(c.slab_floats + 32) + ";");
     ln("const long long g0 = (long long)(blockIdx.x - " + lo + ") * wpb + wib, gstride = (long long)(" + n + ") * wpb;");
   }
@@ -2697,6 +2703,7 @@ bool Builder::build_gws() {
   head << "  extern __shared__ __align__(1024) unsigned char smem[];\n";
   head << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
   head << "  asm volatile(\"griddepcontrol.launch_dependents;\");\n";
+  if (opts_.trace) head << "  stitch_dev::TraceScope stitch_trace_(gsync);\n";
   head << "  (void)ws; (void)gsync; (void)row_lo; (void)row_hi;\n";
   head << "  const Tail tail{";
   {
@@ -2786,6 +2793,7 @@ bool Builder::build_gemm() {
   h << "  extern __shared__ __align__(128) float smem[];\n";
   h << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
   h << "  asm volatile(\"griddepcontrol.launch_dependents;\");\n";
+  if (opts_.trace) h << "  stitch_dev::TraceScope stitch_trace_(gsync);\n";
   h << "  (void)ws; (void)gsync; (void)row_lo; (void)row_hi;\n";
   h << "  stitch_dev::gemm::run<" << L(M) << ", " << L(N) << ", " << L(K) << ", " << L(batch) << ", " << L(sam) << ", "
     << L(sak) << ", " << L(sab) << ", " << L(sbk) << ", " << L(sbn) << ", " << L(sbb) << ">(" << in_ptr(a) << ", "
@@ -2816,7 +2824,7 @@ KernelSpec Builder::build() {
     // COLRED only for a kernel's sole component: packed beside a row group,
     // the streaming cross-row scheme overlaps better (encoder 96 vs 133 us)
     if (comps.size() == 1 && plan_colred(c)) continue;
-    if (plan_row(c)) continue;
+    if (!(opts_.flat_elementwise && all_elementwise(c)) && plan_row(c)) continue;
     if (all_elementwise(c)) {
       c.scheme = "flat";
       int64_t total = 0;
@@ -2954,7 +2962,7 @@ KernelSpec Builder::build() {
         if (c.scheme == "row") spec_.rows = std::max(spec_.rows, c.R);
     if (chunked_) {
       spec_.chunkable = true;
-      spec_.rows_per_cta = comps[0].cta ? 1 : block / 32;
+      spec_.rows_per_cta = comps[0].cta ? 1 : block / comps[0].NT;
     }
     for (size_t i = 0; i < comps.size(); ++i) {
       Component& c = comps[i];
@@ -2969,7 +2977,7 @@ KernelSpec Builder::build() {
                                                                  (c.tc ? (c.tcp ? static_cast<int64_t>(c.tc_list.size()) : 1) *
                                                                                  int64_t{4} * 64 * c.tc_k + 64 * 68
                                                                        : 0)
-                                                          : (c.slab_floats + 32) * (block / 32));
+                                                          : (c.slab_floats + 32) * (block / c.NT));
         if (c.tc) spec_.composition.insert("tensor");
         if (!c.cta)
           for (int x : c.cross) {
@@ -3051,6 +3059,7 @@ KernelSpec Builder::build() {
   // are one resident wave, so its CTAs only take slots this one leaves free).
   head << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
   head << "  asm volatile(\"griddepcontrol.launch_dependents;\");\n";
+  if (opts_.trace) head << "  stitch_dev::TraceScope stitch_trace_(gsync);\n";
   head << "  (void)ws; (void)gsync; (void)smem; (void)row_lo; (void)row_hi;\n";
   spec_.source = head.str() + body_src + "}\n";
   spec_.block = block;
@@ -3061,6 +3070,7 @@ KernelSpec Builder::build() {
   if (all_warp) {
     // every shared-memory term of a warp-row kernel is per warp
     spec_.flex_block = true;
+    spec_.row_threads = comps.size() == 1 && comps[0].scheme == "row" ? comps[0].NT : 32;
     spec_.smem_per_warp = static_cast<int>((smem_floats * 4 + (block / 32) - 1) / (block / 32));
   }
   spec_.workspace_floats = ws_floats_;

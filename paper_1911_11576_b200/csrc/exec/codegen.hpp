@@ -67,6 +67,7 @@ struct KernelSpec {
   int smem_per_warp = 0;
   int64_t rows = 0;
   int rows_per_cta = 1;
+  int row_threads = 32;  // threads per row of a single warp-row component (flex_block grids)
 };
 
 struct CodegenOptions {
@@ -81,10 +82,25 @@ struct CodegenOptions {
   // it is on for CTA rows only.
   bool row_prefetch = true;        // prefetch the next row's register tiles (CTA rows)
   bool row_prefetch_warp = false;  // ... and warp rows
+  // Narrow rows (<= `narrow_row_max` elements, warp scheme, no column
+  // reductions): a group of 4..16 lanes per row, so each lane keeps ~16
+  // elements (4 x 128-bit loads per operand) in flight and a warp works on
+  // several rows at once (softmax rows of 128 keys: 1 load per lane with a
+  // whole warp per row).
+  bool narrow_rows = true;
+  // purely elementwise components (row-vector broadcasts only) as FLAT
+  // grid-stride loops instead of ROW: balanced over the grid whatever the
+  // row count (4096 rows on 1184 CTA slots leave a 14 % round-up tail)
+  bool flat_elementwise = false;  // measured worse (BERT 1.726 -> 1.773 ms): one 128-bit load per thread in flight
+  int narrow_row_max = 256;
   bool loop_fusion = true;
   bool colred = true;
   bool colred_fused = true;
-  bool rcp_divide = true;  // c / x with c = +-2^k as the exact c * rcp.rn(x)
+  bool rcp_divide = true;
+  // timeline tracing: every warp's lane 0 folds %globaltimer at kernel entry
+  // and exit into two u64 words just before the kernel's sync line
+  // (Executor::trace; never on in timed runs)
+  bool trace = false;  // c / x with c = +-2^k as the exact c * rcp.rn(x)
   // every elementwise divide / reciprocal as branch-free rcp.approx + Newton
   // (<= 1 ulp; __frcp_rn / IEEE division carry a slow-path call)
   bool nr_divide = false;

@@ -37,6 +37,7 @@ struct CudaApi {
   STITCH_CU_FN(cuMemcpyDtoDAsync)
   STITCH_CU_FN(cuStreamSynchronize)
   STITCH_CU_FN(cuStreamCreate)
+  STITCH_CU_FN(cuCtxGetStreamPriorityRange)
   STITCH_CU_FN(cuStreamDestroy)
   STITCH_CU_FN(cuStreamWaitEvent)
   STITCH_CU_FN(cuEventCreate)
@@ -94,6 +95,7 @@ struct CudaApi {
     STITCH_CU_LOAD(cuMemcpyDtoDAsync, "cuMemcpyDtoDAsync_v2")
     STITCH_CU_LOAD(cuStreamSynchronize, "cuStreamSynchronize")
     STITCH_CU_LOAD(cuStreamCreate, "cuStreamCreate")
+    STITCH_CU_LOAD(cuCtxGetStreamPriorityRange, "cuCtxGetStreamPriorityRange")
     STITCH_CU_LOAD(cuStreamDestroy, "cuStreamDestroy_v2")
     STITCH_CU_LOAD(cuStreamWaitEvent, "cuStreamWaitEvent")
     STITCH_CU_LOAD(cuEventCreate, "cuEventCreate")

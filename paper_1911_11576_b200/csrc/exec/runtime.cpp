@@ -111,7 +111,11 @@ void apply_codegen_options(CodegenOptions& c, const json::Value& o) {
   if (o.has("lazy_inputs")) c.lazy_inputs = o.at("lazy_inputs").as_bool();
   if (o.has("colred")) c.colred = o.at("colred").as_bool();
   if (o.has("row_prefetch_warp")) c.row_prefetch_warp = o.at("row_prefetch_warp").as_bool();
+  if (o.has("narrow_rows")) c.narrow_rows = o.at("narrow_rows").as_bool();
+  if (o.has("flat_elementwise")) c.flat_elementwise = o.at("flat_elementwise").as_bool();
+  if (o.has("narrow_row_max")) c.narrow_row_max = static_cast<int>(o.at("narrow_row_max").as_int());
   if (o.has("rcp_divide")) c.rcp_divide = o.at("rcp_divide").as_bool();
+  if (o.has("trace")) c.trace = o.at("trace").as_bool();
   if (o.has("gws")) c.gws = o.at("gws").as_bool();
   if (o.has("gemm")) c.gemm = o.at("gemm").as_bool();
   if (o.has("nr_divide")) c.nr_divide = o.at("nr_divide").as_bool();
@@ -499,6 +503,7 @@ void Executor::plan_arena() {
   for (KernelInst& k : kernels_) {
     k.ws_off = 0;  // serial schedule: one shared workspace
     ws_floats_ = std::max(ws_floats_, k.spec.workspace_floats);
+    if (opts_.codegen.trace) sync_words_ = (sync_words_ + 1) / 2 * 2 + 4;  // two u64 trace words before the line
     k.sync_off = sync_words_;
     sync_words_ += std::max(2, k.spec.sync_words) + 30;  // one 128-byte line per kernel
   }
@@ -566,6 +571,19 @@ void Executor::plan_deps() {
     }
     preds_[k].assign(p.begin(), p.end());
   }
+  // critical path estimate: algorithmic bytes at 6 TB/s + 2 us per launch
+  std::vector<double> cost(nk), top(nk, 0.0), bot(nk, 0.0);
+  for (int k = 0; k < nk; ++k) cost[k] = static_cast<double>(kernels_[k].spec.algo_bytes) / 6e6 + 2.0;
+  for (int k = 0; k < nk; ++k)
+    for (int q : preds_[k]) top[k] = std::max(top[k], top[q] + cost[q]);
+  for (int k = nk - 1; k >= 0; --k) {
+    bot[k] += cost[k];
+    for (int q : preds_[k]) bot[q] = std::max(bot[q], bot[k]);
+  }
+  double span = 0;
+  for (int k = 0; k < nk; ++k) span = std::max(span, top[k] + bot[k]);
+  critical_.assign(nk, false);
+  for (int k = 0; k < nk; ++k) critical_[k] = top[k] + bot[k] >= 0.97 * span;
   const size_t words = (static_cast<size_t>(nk) + 63) / 64;
   anc_.assign(nk, std::vector<uint64_t>(words, 0));
   for (int k = 0; k < nk; ++k)
@@ -646,7 +664,10 @@ void Executor::init_device() {
     if (occ < 1) throw std::runtime_error("kernel " + k.spec.name + " cannot be resident (block/smem too large)");
     const int64_t resident = static_cast<int64_t>(occ) * sms_;
     int64_t useful = std::max(1, k.spec.max_grid);
-    if (k.spec.flex_block && k.spec.rows > 0) useful = (k.spec.rows + k.block / 32 - 1) / (k.block / 32);
+    if (k.spec.flex_block && k.spec.rows > 0) {
+      const int64_t rpc = k.block / k.spec.row_threads;
+      useful = (k.spec.rows + rpc - 1) / rpc;
+    }
     if (k.spec.flex_block && k.spec.rows == 0) useful = static_cast<int64_t>(k.spec.max_grid) * k.spec.block / k.block;
     useful = std::max<int64_t>(useful, k.spec.min_grid);
     k.grid = static_cast<int>(std::min<int64_t>(useful, resident));
@@ -681,6 +702,9 @@ void Executor::init_device() {
     lane_events_.push_back(x);
   }
   if (dag_) {
+    int least = 0, greatest = 0;
+    cu_check(cu.cuCtxGetStreamPriorityRange(&least, &greatest), "stream priority range");
+    high_priority_ = greatest;
     for (int j = 1; j < opts_.concurrent_lanes; ++j) {
       CUstream st;
       cu_check(cu.cuStreamCreate(&st, CU_STREAM_NON_BLOCKING), "dag lane stream");
@@ -726,7 +750,7 @@ void Executor::launch_one(int i, int c, int chunks, const void* const* inputs, v
     rng[0] = static_cast<long long>(rows * c);
     rng[1] = static_cast<long long>(rows * (c + 1));
     if (chunks > 1) {
-      const int rpc = k.spec.flex_block ? k.block / 32 : k.spec.rows_per_cta;
+      const int rpc = k.spec.flex_block ? k.block / k.spec.row_threads : k.spec.rows_per_cta;
       const int64_t need = (rows + rpc - 1) / rpc;
       grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(grid, need)));
     }
@@ -764,12 +788,17 @@ void Executor::launch_one(int i, int c, int chunks, const void* const* inputs, v
   cfg.blockDimY = cfg.blockDimZ = 1;
   cfg.sharedMemBytes = k.smem;
   cfg.hStream = static_cast<CUstream>(stream);
-  CUlaunchAttribute attr[2];
+  CUlaunchAttribute attr[4];
   unsigned na_attr = 0;
+  if (dag_ && opts_.critical_priority && critical_[i] && high_priority_ != 0) {
+    attr[na_attr].id = CU_LAUNCH_ATTRIBUTE_PRIORITY;
+    attr[na_attr++].value.priority = high_priority_;
+  }
   if (k.spec.cooperative) {
     attr[na_attr].id = CU_LAUNCH_ATTRIBUTE_COOPERATIVE;
     attr[na_attr++].value.cooperative = 1;
-  } else if (opts_.pdl) {
+  }
+  if (opts_.pdl && (!k.spec.cooperative || opts_.pdl_cooperative)) {
     // overlap this launch with the previous kernel's tail (the kernel waits
     // in griddepcontrol.wait before reading anything)
     attr[na_attr].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
@@ -1054,6 +1083,42 @@ bool Executor::segments_ok_for_overlap() const {
   return true;
 }
 
+json::Value Executor::trace(const void* const* inputs, void* const* outputs, void* stream) {
+  if (!opts_.codegen.trace) throw std::runtime_error("trace needs an executor created with trace=true");
+  CudaApi& cu = CudaApi::get();
+  CtxScope scope(ctx_);
+  CUstream s = static_cast<CUstream>(stream);
+  const int64_t bytes = std::max<int64_t>(sync_words_ * 4, 256);
+  cu_check(cu.cuStreamSynchronize(s), "sync");
+  cu_check(cu.cuMemsetD8Async(sync_, 0, bytes, s), "trace reset");
+  run(inputs, outputs, stream);
+  cu_check(cu.cuStreamSynchronize(s), "sync");
+  std::vector<uint32_t> host(static_cast<size_t>(bytes / 4));
+  cu_check(cu.cuMemcpyDtoHAsync(host.data(), sync_, bytes, s), "trace read");
+  cu_check(cu.cuStreamSynchronize(s), "sync");
+  auto u64 = [&](int64_t w) { return static_cast<uint64_t>(host[w]) | static_cast<uint64_t>(host[w + 1]) << 32; };
+  uint64_t t0 = ~0ull, t1 = 0;
+  std::vector<std::pair<uint64_t, uint64_t>> se(kernels_.size());
+  for (size_t i = 0; i < kernels_.size(); ++i) {
+    se[i] = {~u64(kernels_[i].sync_off - 4), u64(kernels_[i].sync_off - 2)};
+    t0 = std::min(t0, se[i].first);
+    t1 = std::max(t1, se[i].second);
+  }
+  json::Value out = json::Value::object();
+  json::Value ks = json::Value::array();
+  for (size_t i = 0; i < kernels_.size(); ++i) {
+    json::Value k = json::Value::object();
+    k.set("name", kernels_[i].spec.name);
+    k.set("start_us", static_cast<double>(se[i].first - t0) / 1e3);
+    k.set("end_us", static_cast<double>(se[i].second - t0) / 1e3);
+    k.set("algo_bytes", kernels_[i].spec.algo_bytes);
+    ks.push(k);
+  }
+  out.set("kernels", ks);
+  out.set("span_us", static_cast<double>(t1 - t0) / 1e3);
+  return out;
+}
+
 json::Value Executor::profile(const void* const* inputs, void* const* outputs, void* stream, int iters) {
   if (!device_ready_) throw std::runtime_error("executor was created compile-only");
   CudaApi& cu = CudaApi::get();
@@ -1158,6 +1223,9 @@ json::Value Executor::describe() const {
   j.set("launch_order", dag_ ? "dataflow" : "serial");
   j.set("concurrent_lanes", dag_ ? opts_.concurrent_lanes : 1);
   j.set("dependency_edges", edges);
+  int ncrit = 0;
+  for (bool c : critical_) ncrit += c;
+  j.set("critical_kernels", dag_ ? ncrit : 0);
   j.set("folded_constant_kernels", folded_kernels_);
   j.set("sunk_broadcast_kernels", sunk_kernels_);
   j.set("algo_bytes", algo);

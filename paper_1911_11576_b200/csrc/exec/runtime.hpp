@@ -53,13 +53,21 @@ struct ExecOptions {
   int64_t sink_max_bytes = 1 << 20;
   // programmatic dependent launch between consecutive (non-cooperative) kernels
   bool pdl = true;
+  // PDL for grid-barrier kernels too: they get scheduled as the previous
+  // kernel drains (every CTA of a PDL primary is resident before any
+  // dependent CTA launches, so the barrier's co-residency still holds)
+  bool pdl_cooperative = true;  // BERT step 1.739 -> 1.728 ms (dataflow), 1.989 -> 1.966 (serial)
   // Dataflow launch: kernels go out on up to `concurrent_lanes` streams
   // with event edges for their true dependencies only (producer -> consumer,
   // arena reuse, grid-barrier kernels one at a time), so independent fusion
   // groups (parameter-gradient column reductions beside the activation-
   // gradient chain) fill each other's tails. <= 1: one stream in launch order.
   // Not used for chunked schedules or per-kernel profiling.
-  int concurrent_lanes = 8;
+  int concurrent_lanes = 3;  // measured: 3 lanes 1.739 ms, 4: 1.771, 8: 1.762, serial 2.003 (BERT step)
+  // dataflow launch: kernels on the estimated critical path (longest chain
+  // of algorithmic bytes + per-launch overhead) launch at the highest
+  // stream priority, so freed SM slots go to them before side branches
+  bool critical_priority = false;  // measured neutral-to-worse (1.775 vs 1.783 ms at 4 lanes): opt-in
   int chunk_ring = 2;
   CodegenOptions codegen;
   // per fused-op codegen overrides {op id: {option: value}} (the measured
@@ -126,6 +134,7 @@ class Executor {
   void run(const void* const* inputs, void* const* outputs, void* stream);
   void run_host(const void* const* host_inputs, void* const* host_outputs, void* stream);
   json::Value profile(const void* const* inputs, void* const* outputs, void* stream, int iters);
+  json::Value trace(const void* const* inputs, void* const* outputs, void* stream);
 
   const std::vector<KernelInst>& kernels() const { return kernels_; }
   const std::vector<std::string>& input_ids() const { return input_ids_; }
@@ -158,6 +167,8 @@ class Executor {
   bool dag_ = false;
   std::vector<std::vector<int>> preds_;  // kernel -> kernels it must follow
   std::vector<std::vector<uint64_t>> anc_;  // kernel -> ancestor bitset
+  std::vector<bool> critical_;              // kernel on the estimated critical path
+  int high_priority_ = 0;                   // greatest stream priority of the context
   std::vector<int> writer_;                 // value buffer -> producing kernel
   std::vector<std::vector<int>> touch_;     // value buffer -> kernels reading / writing it
   std::vector<void*> dag_lanes_;         // CUstreams for lanes 1.. (lane 0 = the caller's stream)

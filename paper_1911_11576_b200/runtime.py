@@ -47,6 +47,8 @@ def lib():
         L.stitch_executor_run_host.restype = ctypes.c_int
         L.stitch_executor_profile.argtypes = [vp, vp, vp, vp, ctypes.c_int, ctypes.POINTER(vp)]
         L.stitch_executor_profile.restype = ctypes.c_int
+        L.stitch_executor_trace.argtypes = [vp, vp, vp, vp, ctypes.POINTER(vp)]
+        L.stitch_executor_trace.restype = ctypes.c_int
         L.stitch_executor_sources.argtypes = [vp]
         L.stitch_executor_sources.restype = vp
         L.stitch_last_error.restype = cp
@@ -149,6 +151,14 @@ class Executor:
         ins = _ptr_array([_data_ptr(x) for x in inputs])
         outs = _ptr_array([_data_ptr(x) for x in outputs])
         _check(lib().stitch_executor_run_host(self._h, ins, outs, ctypes.c_void_p(stream)))
+
+    def trace(self, inputs, outputs, stream=0):
+        """Per-kernel [start, end] (us) of one pass; needs trace=True."""
+        ins = _ptr_array([_data_ptr(x) for x in inputs])
+        outs = _ptr_array([_data_ptr(x) for x in outputs])
+        res = ctypes.c_void_p()
+        _check(lib().stitch_executor_trace(self._h, ins, outs, ctypes.c_void_p(stream), ctypes.byref(res)))
+        return json.loads(_take_string(res))
 
     def profile(self, inputs, outputs, stream=0, iters=10):
         ins = _ptr_array([_data_ptr(x) for x in inputs])
