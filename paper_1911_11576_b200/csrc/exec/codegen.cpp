@@ -161,7 +161,7 @@ class Builder {
 
   void emit_flat(const Component& c, const std::string& lo, const std::string& n);
   void emit_row(Component& c, const std::string& lo, const std::string& n, const std::string& cta_rank);
-  void emit_row_finalize(std::vector<Component*>& comps);
+  void emit_row_finalize(std::vector<Component*>& comps, bool split);
   void emit_sectioned(const std::vector<int>& members);
   // BLOCK: heterogeneous groups over a common leading index G (paper Fig. 1:
   // dots + reductions + elementwise over different inner index spaces), one
@@ -210,6 +210,7 @@ class Builder {
   bool uses_barrier_ = false;
   std::map<int, int64_t> ws_off_;  // value -> workspace offset (floats)
   std::map<int, std::string> cross_parts_;  // cross value -> nparts expression
+  std::string fin_body_;  // split_cross: body of the column-reduction fold kernel
   bool chunked_ = false;  // the single ROW component runs rows [row_lo, row_hi) (launch-time chunking)
 };
 
@@ -2114,12 +2115,17 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
   close();
 }
 
-void Builder::emit_row_finalize(std::vector<Component*>& comps) {
+void Builder::emit_row_finalize(std::vector<Component*>& comps, bool split) {
   bool any = false;
   for (Component* c : comps) any = any || !c->cross.empty();
   if (!any) return;
-  uses_barrier_ = true;
-  ln("stitch_dev::grid_barrier(gsync);");
+  if (split) {
+    ln("// partials of every CTA of the row kernel are complete (this kernel");
+    ln("// runs after it); row_lo = their count");
+  } else {
+    uses_barrier_ = true;
+    ln("stitch_dev::grid_barrier(gsync);");
+  }
   ln("// deterministic combine of the per-CTA partials: every (output, column");
   ln("// block) item of every cross output in ONE grid-stride loop, so all CTAs");
   ln("// work at once (not one output after another on So / 32 CTAs)");
@@ -2187,6 +2193,7 @@ void Builder::emit_row_finalize(std::vector<Component*>& comps) {
   bool any_post = false;
   for (Component* c : comps) any_post = any_post || !c->post.empty();
   if (!any_post) return;
+  if (split) throw InternalError("split cross finalize with post-reduction ops");
   ln("stitch_dev::grid_barrier(gsync);");
   for (Component* c : comps)
     for (int p : c->post) {
@@ -3013,11 +3020,44 @@ KernelSpec Builder::build() {
       memo_.pop_back();
       if (ranged) close();
     }
-    for (Component* c : rowc)
-      if (!c->cross.empty()) smem_floats = std::max<int64_t>(smem_floats, block);
-    memo_.emplace_back();
-    emit_row_finalize(rowc);
-    memo_.pop_back();
+    bool split = opts_.split_cross && comps.size() == 1 && comps[0].scheme == "row" && !comps[0].cross.empty() &&
+                 comps[0].post.empty();
+    if (split)
+      for (int x : comps[0].cross) split = split && vals_[x].output;
+    if (split) {
+      // the fold goes to its own kernel (KernelSpec::fin_*), emitted into a
+      // separate buffer; the partial count arrives as row_lo
+      for (int x : comps[0].cross) cross_parts_[x] = "(int)row_lo";
+      std::ostringstream fin;
+      std::swap(out_, fin);
+      const int saved_indent = indent_;
+      indent_ = 1;
+      memo_.emplace_back();
+      open("");
+      emit_row_finalize(rowc, true);
+      close();
+      memo_.pop_back();
+      indent_ = saved_indent;
+      std::swap(out_, fin);
+      fin_body_ = fin.str();
+      for (int x : comps[0].cross) spec_.fin_outputs.push_back(vals_[x].id);
+      spec_.fin_smem_bytes = 256 * 4 + 16;
+      int64_t items = 0;
+      for (int x : comps[0].cross) {
+        const int in = vals_[x].operands[0];
+        const bool scalar = static_cast<int>(vals_[x].node->reduce_dims.size()) == static_cast<int>(vals_[in].dims.size());
+        const int64_t So = scalar ? 1 : prod(vals_[in].dims, comps[0].k);
+        items += (So + (So >= 32 ? 31 : 0)) / (So >= 32 ? 32 : 1);
+      }
+      spec_.fin_max_grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(items, 1 << 20)));
+      spec_.cooperative = false;  // no grid barrier left in the row kernel
+    } else {
+      for (Component* c : rowc)
+        if (!c->cross.empty()) smem_floats = std::max<int64_t>(smem_floats, block);
+      memo_.emplace_back();
+      emit_row_finalize(rowc, false);
+      memo_.pop_back();
+    }
     spec_.max_grid = std::max<int>(spec_.max_grid, static_cast<int>(comps.size()));
     if (comps.size() > 1 && !opts_.pack_sequential) spec_.min_grid = static_cast<int>(comps.size());
     spec_.scheme = scheme;
@@ -3062,6 +3102,19 @@ KernelSpec Builder::build() {
   if (opts_.trace) head << "  stitch_dev::TraceScope stitch_trace_(gsync);\n";
   head << "  (void)ws; (void)gsync; (void)smem; (void)row_lo; (void)row_hi;\n";
   spec_.source = head.str() + body_src + "}\n";
+  if (!fin_body_.empty()) {
+    spec_.fin_name = name_ + "_fold";
+    std::ostringstream fh;
+    fh << "// column-reduction fold of fused op '" << name_ << "': fixed-order combine of the per-CTA partials "
+       << name_ << " wrote to the workspace\n";
+    fh << "extern \"C\" __global__ void __launch_bounds__(256) " << spec_.fin_name << "(" << join(params, ", ") << ") {\n";
+    fh << "  extern __shared__ __align__(128) float smem[];\n";
+    fh << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
+    fh << "  asm volatile(\"griddepcontrol.launch_dependents;\");\n";
+    if (opts_.trace) fh << "  stitch_dev::TraceScope stitch_trace_(gsync);\n";
+    fh << "  (void)ws; (void)gsync; (void)smem; (void)row_lo; (void)row_hi;\n";
+    spec_.fin_source = fh.str() + fin_body_ + "}\n";
+  }
   spec_.block = block;
   spec_.smem_bytes = static_cast<int>(smem_floats * 4 + (smem_floats ? 16 : 0));
   bool all_warp = !sectioned;

@@ -68,6 +68,15 @@ struct KernelSpec {
   int64_t rows = 0;
   int rows_per_cta = 1;
   int row_threads = 32;  // threads per row of a single warp-row component (flex_block grids)
+  // split_cross: the fixed-order combine of the per-CTA column partials runs
+  // as a second kernel `fin_name` (same arguments; row_lo = the partial count,
+  // i.e. this kernel's grid) -- no grid barrier, so this kernel is not
+  // cooperative and its row outputs release their consumers before the
+  // column reductions are folded. fin_outputs: the outputs it writes.
+  std::string fin_name, fin_source;
+  int fin_max_grid = 0;
+  int fin_smem_bytes = 0;
+  std::vector<std::string> fin_outputs;
 };
 
 struct CodegenOptions {
@@ -91,7 +100,10 @@ struct CodegenOptions {
   // purely elementwise components (row-vector broadcasts only) as FLAT
   // grid-stride loops instead of ROW: balanced over the grid whatever the
   // row count (4096 rows on 1184 CTA slots leave a 14 % round-up tail)
-  bool flat_elementwise = false;  // measured worse (BERT 1.726 -> 1.773 ms): one 128-bit load per thread in flight
+  bool flat_elementwise = false;
+  // cross-row (column) reductions of a row group folded by a separate
+  // dependent kernel instead of after a grid barrier (KernelSpec::fin_*)
+  bool split_cross = true;  // measured worse (BERT 1.726 -> 1.773 ms): one 128-bit load per thread in flight
   int narrow_row_max = 256;
   bool loop_fusion = true;
   bool colred = true;

@@ -113,6 +113,7 @@ void apply_codegen_options(CodegenOptions& c, const json::Value& o) {
   if (o.has("row_prefetch_warp")) c.row_prefetch_warp = o.at("row_prefetch_warp").as_bool();
   if (o.has("narrow_rows")) c.narrow_rows = o.at("narrow_rows").as_bool();
   if (o.has("flat_elementwise")) c.flat_elementwise = o.at("flat_elementwise").as_bool();
+  if (o.has("split_cross")) c.split_cross = o.at("split_cross").as_bool();
   if (o.has("narrow_row_max")) c.narrow_row_max = static_cast<int>(o.at("narrow_row_max").as_int());
   if (o.has("rcp_divide")) c.rcp_divide = o.at("rcp_divide").as_bool();
   if (o.has("trace")) c.trace = o.at("trace").as_bool();
@@ -365,15 +366,58 @@ void Executor::build_kernels() {
       auto pos = std::find(tup.operands.begin(), tup.operands.end(), o) - tup.operands.begin();
       k.out_bufs.push_back(buffer(out_keys.at(pos), body.at(o).shape.byte_count()));
     }
+    k.reads = k.in_bufs;
+    k.writes = k.out_bufs;
+    if (!k.spec.fin_source.empty()) {
+      // split_cross: the row kernel writes its row outputs, the fold kernel
+      // (next in launch order) the column reductions from the partials
+      KernelInst f;
+      f.op_id = id;
+      f.variant = k.variant;
+      f.spec = k.spec;
+      f.spec.name = k.spec.fin_name;
+      f.spec.source = k.spec.fin_source;
+      f.spec.fin_source.clear();
+      f.spec.scheme = "fold(" + std::to_string(k.spec.fin_outputs.size()) + " column reductions of " + k.spec.name + ")";
+      f.spec.composition = {"block"};
+      f.spec.block = 256;
+      f.spec.max_grid = k.spec.fin_max_grid;
+      f.spec.min_grid = 1;
+      f.spec.cooperative = false;
+      f.spec.smem_bytes = k.spec.fin_smem_bytes;
+      f.spec.sync_words = 0;
+      f.spec.chunkable = false;
+      f.spec.flex_block = false;
+      f.spec.cluster = 0;
+      f.spec.tma.clear();
+      f.spec.rows = 0;
+      f.spec.algo_bytes = 0;  // partials only; the group's bytes are counted on the row kernel
+      f.in_bufs = k.in_bufs;
+      f.out_bufs = k.out_bufs;
+      f.reads = k.in_bufs;
+      std::set<std::string> folded(k.spec.fin_outputs.begin(), k.spec.fin_outputs.end());
+      k.writes.clear();
+      for (size_t j = 0; j < k.out_bufs.size(); ++j) {
+        if (folded.count(k.spec.outputs[j]))
+          f.writes.push_back(k.out_bufs[j]);
+        else
+          k.writes.push_back(k.out_bufs[j]);
+      }
+      f.reads.insert(f.reads.end(), k.writes.begin(), k.writes.end());  // kept alive (passed, not read)
+      f.fold_of = static_cast<int>(kernels_.size());
+      kernels_.push_back(std::move(k));
+      kernels_.push_back(std::move(f));
+      continue;
+    }
     kernels_.push_back(std::move(k));
   }
   // Lifetimes.
   for (size_t ki = 0; ki < kernels_.size(); ++ki) {
-    for (int b : kernels_[ki].out_bufs) {
+    for (int b : kernels_[ki].writes) {
       if (bufs_[b].first >= 0) throw InternalError("value produced twice: " + bufs_[b].key);
       bufs_[b].first = bufs_[b].last = static_cast<int>(ki);
     }
-    for (int b : kernels_[ki].in_bufs) {
+    for (int b : kernels_[ki].reads) {
       if (bufs_[b].kind == ValueBuf::kInput) continue;
       if (bufs_[b].first < 0) throw InternalError("value consumed before it is produced: " + bufs_[b].key);
       bufs_[b].last = std::max(bufs_[b].last, static_cast<int>(ki));
@@ -461,7 +505,7 @@ void Executor::plan_chunks() {
         // no chunk ring is placed on top of a value a later chunk still
         // writes or reads.
         for (int k = seg.first; k <= seg.last; ++k) {
-          for (const std::vector<int>* v : {&kernels_[k].in_bufs, &kernels_[k].out_bufs})
+          for (const std::vector<int>* v : {&kernels_[k].reads, &kernels_[k].writes})
             for (int b : *v) {
               bufs_[b].first = std::min(bufs_[b].first, seg.first);
               bufs_[b].last = std::max(bufs_[b].last, seg.last);
@@ -525,6 +569,10 @@ void Executor::plan_arena() {
       off = std::max(off, (hi + 63) / 64 * 64);
     }
     kernels_[k].ws_off = need > 0 ? off : 0;
+    if (kernels_[k].fold_of >= 0) {  // reads the partials its row kernel (the previous index) left there
+      kernels_[k].ws_off = kernels_[kernels_[k].fold_of].ws_off;
+      continue;
+    }
     ws_floats_ = std::max(ws_floats_, off + need);
   }
   // invariant: values sharing arena bytes are ordered by true dependencies
@@ -550,18 +598,19 @@ void Executor::plan_deps() {
   writer_.assign(bufs_.size(), -1);
   touch_.assign(bufs_.size(), {});
   for (int k = 0; k < nk; ++k) {
-    for (int b : kernels_[k].out_bufs) {
+    for (int b : kernels_[k].writes) {
       writer_[b] = k;
       touch_[b].push_back(k);
     }
-    for (int b : kernels_[k].in_bufs) touch_[b].push_back(k);
+    for (int b : kernels_[k].reads) touch_[b].push_back(k);
   }
   if (!dag_) return;
   int last_coop = -1;
   for (int k = 0; k < nk; ++k) {
     std::set<int> p;
-    for (int b : kernels_[k].in_bufs)  // read after write
+    for (int b : kernels_[k].reads)  // read after write
       if (writer_[b] >= 0 && writer_[b] != k) p.insert(writer_[b]);
+    if (kernels_[k].fold_of >= 0) p.insert(kernels_[k].fold_of);  // partials in the workspace
     // grid-barrier kernels spin until every CTA is resident: never two in
     // flight (every other kernel in flight runs to completion unconditionally,
     // and PDL dependents launch only once all of their primary's CTAs run)
@@ -755,6 +804,7 @@ void Executor::launch_one(int i, int c, int chunks, const void* const* inputs, v
       grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(grid, need)));
     }
   }
+  if (k.fold_of >= 0) rng[0] = kernels_[k.fold_of].grid;  // partial count
   args[na] = &rng[0];
   args[na + 1] = &rng[1];
   // gws scheme: tensor maps of the operand tiles, by value after row_lo/row_hi
@@ -1030,7 +1080,7 @@ void Executor::run_host(const void* const* host_inputs, void* const* host_output
   // output slot -> producing kernel
   std::vector<int> producer(no, -1);
   for (size_t k = 0; k < kernels_.size(); ++k)
-    for (int b : kernels_[k].out_bufs)
+    for (int b : kernels_[k].writes)
       if (bufs_[b].kind == ValueBuf::kOutput) producer[bufs_[b].slot] = static_cast<int>(k);
   std::vector<std::vector<int>> outs_of(kernels_.size());
   for (size_t o = 0; o < no; ++o)
@@ -1203,6 +1253,7 @@ json::Value Executor::describe() const {
     e.set("inputs", json::Value::array_of(k.spec.inputs));
     e.set("outputs", json::Value::array_of(k.spec.outputs));
     e.set("cache_hit", k.cache_hit);
+    if (k.fold_of >= 0) e.set("fold_of", kernels_[k.fold_of].spec.name);
     algo += k.spec.algo_bytes;
     ks.push(e);
   }

@@ -112,7 +112,12 @@ struct KernelInst {
   std::vector<TmapBytes> tmaps;
   std::vector<unsigned long long> tmap_ptrs;
   std::string op_id;                 // fused op or unfused op id in the fused graph
-  std::vector<int> in_bufs, out_bufs;
+  std::vector<int> in_bufs, out_bufs;  // pointer arguments, in order
+  // buffers this launch reads / writes (dependencies, lifetimes): = in_bufs /
+  // out_bufs, except for a split row kernel and its fold (split_cross), which
+  // share one argument list but write disjoint outputs
+  std::vector<int> reads, writes;
+  int fold_of = -1;                  // fold kernel: index of the row kernel whose partials it combines
   void* module = nullptr;            // CUmodule
   void* fn = nullptr;                // CUfunction
   int grid = 1;
