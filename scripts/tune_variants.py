@@ -54,7 +54,12 @@ VARIANTS = [
     {"nr_divide": True, "min_ctas_per_sm": 3},
     {"nr_divide": True, "loop_fusion": False},
     {"nr_divide": True, "wide_cross_cta": True, "wide_cross_threads": 192},
+    {"narrow_rows": False},
 ]
+# Not candidates: split_cross (one kernel + grid barrier instead of a row
+# kernel and its fold). Timed alone the single kernel wins, inside the
+# dataflow step the split wins (its fold leaves the critical path: BERT
+# 1.732 -> 1.602 ms), so it is decided on the whole step, not per kernel.
 
 
 def main():
@@ -97,8 +102,12 @@ def main():
         for _ in range(a.reps):
             flush_l2()
             prof = ex.profile(ins, outs, stream=s.cuda_stream, iters=1)
+            per_op = {}  # a split row group's row kernel + fold count together
             for k in prof["kernels"]:
-                acc.setdefault(k["op"] if "op" in k else k["name"], []).append(k["us"])
+                op = k["op"] if "op" in k else k["name"]
+                per_op[op] = per_op.get(op, 0.0) + k["us"]
+            for op, us in per_op.items():
+                acc.setdefault(op, []).append(us)
         times[vi] = {op: float(np.median(us)) for op, us in acc.items()}
         print("variant %-55s total %8.1f us  (%.0f s)" % (json.dumps(v), sum(times[vi].values()), time.time() - t0),
               flush=True)
