@@ -825,10 +825,13 @@ bool Builder::plan_row(Component& c) {
     wide_cross = n_cross * ((max_inner + 31) / 32) > 48;
     c.cta = wide_cross;
   }
+  const bool forced_cta = !c.cta && opts_.cta_rows > 0 && max_inner >= opts_.cta_rows;
+  if (forced_cta) c.cta = true;
   if (c.cta) {
     int nt = 256;
     if (max_inner > 4096) nt = 512;
     if (max_inner > 8192) nt = 1024;
+    if (forced_cta) nt = opts_.cta_rows;
     // wide multi-gradient rows: a small CTA (2 warps for 768 columns) per
     // row -- ~12 columns per thread, cheap 64-thread barriers, many rows
     // in flight per SM

@@ -103,7 +103,11 @@ struct CodegenOptions {
   bool flat_elementwise = false;
   // cross-row (column) reductions of a row group folded by a separate
   // dependent kernel instead of after a grid barrier (KernelSpec::fin_*)
-  bool split_cross = true;  // measured worse (BERT 1.726 -> 1.773 ms): one 128-bit load per thread in flight
+  bool split_cross = true;
+  // > 0: a CTA of this many threads per row for row groups that would run a
+  // warp per row (register-heavy multi-layer groups: more warps resident,
+  // fewer values per thread); a per-group tuning candidate
+  int cta_rows = 0;  // measured worse (BERT 1.726 -> 1.773 ms): one 128-bit load per thread in flight
   int narrow_row_max = 256;
   bool loop_fusion = true;
   bool colred = true;

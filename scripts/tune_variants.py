@@ -55,6 +55,10 @@ VARIANTS = [
     {"nr_divide": True, "loop_fusion": False},
     {"nr_divide": True, "wide_cross_cta": True, "wide_cross_threads": 192},
     {"narrow_rows": False},
+    {"cta_rows": 128},
+    {"cta_rows": 192},
+    {"cta_rows": 256},
+    {"cta_rows": 192, "loop_fusion": False},
 ]
 # Not candidates: split_cross (one kernel + grid barrier instead of a row
 # kernel and its fold). Timed alone the single kernel wins, inside the

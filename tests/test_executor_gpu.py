@@ -215,7 +215,9 @@ def test_gru_double_buffer_and_prefetch_variants():
 VARIANTS = [dict(pack_sequential=True), dict(loop_fusion=False), dict(row_prefetch=False), dict(row_prefetch_warp=True),
             dict(tma_double_buffer=True), dict(tensor_cores=True, gws=False), dict(colred=False), dict(lazy_inputs=True),
             dict(gws=False), dict(gws=False, tma_double_buffer=True),
-            dict(pdl=False), dict(fold_constants=False), dict(colred_cp_async=False), dict(colred_cols=128), dict(cross_smem=False), dict(tma_early=True)]
+            dict(pdl=False), dict(fold_constants=False), dict(colred_cp_async=False), dict(colred_cols=128), dict(cross_smem=False), dict(tma_early=True),
+            dict(split_cross=False), dict(narrow_rows=False), dict(cta_rows=192), dict(cta_rows=128),
+            dict(concurrent_lanes=1), dict(critical_priority=True), dict(flat_elementwise=True), dict(pdl_cooperative=False)]
 
 
 @pytest.mark.parametrize("name", list(W.CONFIGS))
@@ -539,7 +541,9 @@ def test_bert_bench_plan_anchored_parity():
     g = W.bert(batch=8)
     fused = tuning.plan_like("bert", g)
     ins = orc.random_inputs(g, seed=83)
-    ex, got = run_device(fused, ins)
+    # the bench's per-group variant table too (what bench.py runs)
+    ex, got = run_device(fused, ins, kernel_options=tuning.kernel_variants("bert"))
+    assert any(k["variant"] for k in ex.info["kernels"])
     outs = orc.graph_outputs(g)
     assert len(outs) == len(got) == 182
     by_id = dict(zip(outs, got))
