@@ -211,6 +211,7 @@ class Builder {
   std::map<int, int64_t> ws_off_;  // value -> workspace offset (floats)
   std::map<int, std::string> cross_parts_;  // cross value -> nparts expression
   std::string fin_body_;  // split_cross: body of the column-reduction fold kernel
+  size_t n_comps_ = 1;    // components of the kernel being emitted
   bool chunked_ = false;  // the single ROW component runs rows [row_lo, row_hi) (launch-time chunking)
 };
 
@@ -2053,6 +2054,27 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
     }
     release_at.clear();
   }
+  {
+    // dead intermediates: drop this row's lines from L2 without write-back
+    std::vector<int> dead;
+    for (int v : inputs_)
+      if (n_comps_ == 1 && opts_.discard_inputs.count(vals_[v].id) && c.cls[v] == Cls::kRowed && prod(vals_[v].dims, k) * 4 % 128 == 0)
+        dead.push_back(v);
+    if (!dead.empty()) {
+      if (c.cta)
+        ln("__syncthreads();  // every thread is done with this row's inputs");
+      else if (NT == 32)
+        ln("__syncwarp();  // every lane is done with this row's inputs");
+      else
+        ln("__syncwarp(((1u << " + std::to_string(NT) + ") - 1u) << ((threadIdx.x & 31) & ~" + std::to_string(NT - 1) +
+           "));  // the row group is done with this row's inputs");
+      for (int v : dead) {
+        const int64_t So = prod(vals_[v].dims, k);
+        ln("for (int l = t; l < " + std::to_string(So * 4 / 128) + "; l += " + std::to_string(NT) + ") stitch_dev::discard_l2(" +
+           in_ptr(v) + " + row * " + std::to_string(So) + "LL + l * 32);  // " + vals_[v].id + " (dead after this kernel)");
+      }
+    }
+  }
   close();  // row loop
   if (c.tc) ln("stitch_dev::tc::dealloc(tmem, " + std::string(c.tcp ? (c.tc_list.size() > 1 ? "256" : "128") : "64") + ");");
 
@@ -2964,6 +2986,7 @@ KernelSpec Builder::build() {
     }
     std::vector<Component*> rowc;
     std::string scheme;
+    n_comps_ = comps.size();
     chunked_ = comps.size() == 1 && comps[0].scheme == "row" && comps[0].cross.empty() && comps[0].post.empty() &&
                comps[0].free_out.empty();
     if (comps.size() == 1 && comps[0].scheme == "row") spec_.rows = comps[0].R;

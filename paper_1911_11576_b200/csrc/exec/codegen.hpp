@@ -107,7 +107,14 @@ struct CodegenOptions {
   // > 0: a CTA of this many threads per row for row groups that would run a
   // warp per row (register-heavy multi-layer groups: more warps resident,
   // fewer values per thread); a per-group tuning candidate
-  int cta_rows = 0;  // measured worse (BERT 1.726 -> 1.773 ms): one 128-bit load per thread in flight
+  int cta_rows = 0;
+  // Row-scheme inputs (body parameter ids) whose only reader is this kernel
+  // and that are not graph outputs (arena intermediates): after a row is
+  // consumed its 128-byte lines are invalidated in L2 (discard.global.L2),
+  // so dirty lines the producer left there are never written back to HBM.
+  // Filled per kernel by the executor when `l2_discard` is on.
+  std::set<std::string> discard_inputs;
+  bool l2_discard = true;  // measured worse (BERT 1.726 -> 1.773 ms): one 128-bit load per thread in flight
   int narrow_row_max = 256;
   bool loop_fusion = true;
   bool colred = true;

@@ -115,6 +115,7 @@ void apply_codegen_options(CodegenOptions& c, const json::Value& o) {
   if (o.has("flat_elementwise")) c.flat_elementwise = o.at("flat_elementwise").as_bool();
   if (o.has("split_cross")) c.split_cross = o.at("split_cross").as_bool();
   if (o.has("cta_rows")) c.cta_rows = static_cast<int>(o.at("cta_rows").as_int());
+  if (o.has("l2_discard")) c.l2_discard = o.at("l2_discard").as_bool();
   if (o.has("narrow_row_max")) c.narrow_row_max = static_cast<int>(o.at("narrow_row_max").as_int());
   if (o.has("rcp_divide")) c.rcp_divide = o.at("rcp_divide").as_bool();
   if (o.has("trace")) c.trace = o.at("trace").as_bool();
@@ -241,6 +242,14 @@ void Executor::build_kernels() {
         sink_src[id] = n.operands[0];
     }
   std::map<std::string, std::string> names;
+  struct Regen {  // what generated each kernel (L2-discard second pass)
+    size_t ki;
+    Graph body;
+    std::string kname;
+    std::map<std::string, double> consts;
+    CodegenOptions co;
+  };
+  std::vector<Regen> regen;
   for (const std::string& id : topo) {
     const OpNode& n = g_.at(id);
     if (n.type != OpType::kFused && !is_fusible(n)) continue;
@@ -358,6 +367,7 @@ void Executor::build_kernels() {
       k.variant = opts_.kernel_options.at(id);
     }
     k.spec = generate_kernel(body, kname, consts, co);
+    if (co.l2_discard) regen.push_back({kernels_.size(), body, kname, consts, co});
     const OpNode& tup = body.at(body.outputs.front());
     for (const std::string& in : k.spec.inputs) {
       const std::string& outer = outer_of.at(in);
@@ -411,6 +421,40 @@ void Executor::build_kernels() {
       continue;
     }
     kernels_.push_back(std::move(k));
+  }
+  // L2 discard: an arena value (not a graph output) read by exactly one
+  // kernel is dead once that kernel has consumed a row of it; regenerate
+  // those consumers with the value in their discard set.
+  if (!regen.empty()) {
+    std::set<std::string> out_keys_all;
+    for (const std::string& o : output_ids_) {
+      const OpNode& n = g_.at(o);
+      out_keys_all.insert(n.type == OpType::kGetElement ? n.operands[0] + "#" + std::to_string(n.tuple_index)
+                          : n.type == OpType::kFused    ? o + "#0"
+                                                        : o);
+    }
+    std::vector<int> readers(bufs_.size(), 0), produced(bufs_.size(), 0);
+    for (const KernelInst& k : kernels_) {
+      if (k.fold_of >= 0) continue;  // a fold passes the pointers but reads only its partials
+      std::set<int> r(k.in_bufs.begin(), k.in_bufs.end());
+      for (int b : r) ++readers[b];
+      for (int b : k.writes) ++produced[b];
+    }
+    for (Regen& rg : regen) {
+      KernelInst& k = kernels_[rg.ki];
+      std::set<std::string> dead;
+      for (size_t j = 0; j < k.in_bufs.size(); ++j) {
+        const int b = k.in_bufs[j];
+        if (bufs_[b].kind == ValueBuf::kArena && produced[b] == 1 && readers[b] == 1 && !out_keys_all.count(bufs_[b].key))
+          dead.insert(k.spec.inputs[j]);
+      }
+      if (dead.empty()) continue;
+      rg.co.discard_inputs = dead;
+      KernelSpec spec = generate_kernel(rg.body, rg.kname, rg.consts, rg.co);
+      if (spec.inputs != k.spec.inputs || spec.outputs != k.spec.outputs || spec.fin_name != k.spec.fin_name)
+        throw InternalError("L2-discard regeneration changed kernel " + rg.kname + "'s arguments");
+      k.spec = std::move(spec);
+    }
   }
   // Lifetimes.
   for (size_t ki = 0; ki < kernels_.size(); ++ki) {

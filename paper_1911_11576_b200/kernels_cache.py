@@ -89,9 +89,11 @@ def prebuild(verbose=True, workers=None):
     jobs = []
     for tag, fused in plans():
         opts = {"chunking": False, "fold_constants": False, "sink_broadcasts": False} if tag.endswith("/unfused") else {}
-        if tag.endswith("/bench"):
+        if tag.endswith("/bench") or tag.endswith("/bench-groups"):
             opts["kernel_options"] = tuning.kernel_variants(tag.split("/")[0])
         jobs.append((json.dumps(fused), opts))
+        if tag.endswith("/unfused"):  # bench.py's folded unfused context line
+            jobs.append((json.dumps(fused), {"chunking": False}))
     n = hits = 0
     with cf.ProcessPoolExecutor(workers or max(1, min(16, os.cpu_count() or 1))) as pool:
         for a, b in pool.map(_compile, jobs):

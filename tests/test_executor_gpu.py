@@ -720,3 +720,28 @@ def test_dataflow_launch_bit_identical(case):
         torch.cuda.synchronize()
         for k, (a, b) in enumerate(zip(ref, d_out)):
             assert np.array_equal(a, b.cpu().numpy()), (rep, ex.output_ids[k])
+
+
+def test_l2_discard_bit_identical():
+    """L2 discard of dead intermediates (an arena value read by one kernel
+    has its 128-byte lines invalidated once that kernel consumed the row):
+    the bench's BERT groups give bit-identical results with and without it,
+    over repeated graph replays (a line dropped while still needed would
+    read back as garbage)."""
+    g = W.bert(batch=8)
+    fused = tuning.plan_like("bert", g)
+    kw = dict(kernel_options=tuning.kernel_variants("bert"))
+    rng = np.random.default_rng(73)
+    nodes = {n["id"]: n for n in g["nodes"]}
+    ins = {i: rng.standard_normal(nodes[i]["shape"]["dims"], dtype=np.float32) for i in orc.graph_inputs(g)}
+    _, ref = run_device(fused, ins, l2_discard=False, **kw)
+    ex = rt.Executor(fused, device=0, **kw)
+    assert any("discard_l2(" in s.split('extern "C"')[-1] for s in ex.sources().values())
+    d_in = [torch.from_numpy(np.ascontiguousarray(ins[i])).cuda() for i in ex.input_ids]
+    d_out = [torch.empty(t["dims"], dtype=torch.float32, device="cuda") for t in ex.info["outputs"]]
+    s = torch.cuda.Stream()
+    for rep in range(3):
+        ex.run(d_in, d_out, stream=s.cuda_stream)
+        torch.cuda.synchronize()
+        for k, (a, b) in enumerate(zip(ref, d_out)):
+            assert np.array_equal(a, b.cpu().numpy()), (rep, ex.output_ids[k])
