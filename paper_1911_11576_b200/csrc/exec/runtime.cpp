@@ -764,7 +764,10 @@ void Executor::init_device() {
     }
     if (k.spec.flex_block && k.spec.rows == 0) useful = static_cast<int64_t>(k.spec.max_grid) * k.spec.block / k.block;
     useful = std::max<int64_t>(useful, k.spec.min_grid);
-    k.grid = static_cast<int>(std::min<int64_t>(useful, resident));
+    int64_t cap = resident;
+    if (dag_ && opts_.grid_fraction < 1.0 && !k.spec.cooperative)
+      cap = std::max<int64_t>(sms_, static_cast<int64_t>(static_cast<double>(resident) * opts_.grid_fraction));
+    k.grid = static_cast<int>(std::min<int64_t>(useful, cap));
     if (k.grid < k.spec.min_grid)
       throw std::runtime_error("kernel " + k.spec.name + ": packed components need " + std::to_string(k.spec.min_grid) +
                                " resident CTAs");
@@ -930,6 +933,21 @@ void Executor::launch_dag(const void* const* inputs, void* const* outputs, void*
   for (int k = 0; k < nk; ++k) {
     const std::vector<int>& pk = preds_[k];
     int lane = -1;
+    if (opts_.big_lane_bytes > 0 && nl > 1) {
+      if (kernels_[k].spec.algo_bytes >= opts_.big_lane_bytes) {
+        lane = 0;
+      } else {
+        for (int l = 1; l < nl && lane < 0; ++l)
+          if (!pk.empty() && tail[l] == pk.back()) lane = l;
+        for (int l = 1; l < nl && lane < 0; ++l)
+          if (!used[l]) lane = l;
+        if (lane < 0) {
+          lane = 1;
+          for (int l = 2; l < nl; ++l)
+            if (tail[l] < tail[lane]) lane = l;
+        }
+      }
+    }
     for (int l = 0; l < nl && lane < 0; ++l)
       if (!pk.empty() && tail[l] == pk.back()) lane = l;
     if (lane < 0 && tail[0] < 0) lane = 0;

@@ -67,7 +67,16 @@ struct ExecOptions {
   // dataflow launch: kernels on the estimated critical path (longest chain
   // of algorithmic bytes + per-launch overhead) launch at the highest
   // stream priority, so freed SM slots go to them before side branches
-  bool critical_priority = false;  // measured neutral-to-worse (1.775 vs 1.783 ms at 4 lanes): opt-in
+  bool critical_priority = false;
+  // > 0: kernels moving at least this many algorithmic bytes all go to lane
+  // 0 (back to back, PDL-chained); smaller ones spread over the other lanes
+  // and fill the big kernels' ramps and tails. 0: lane of the latest
+  // predecessor, else a fresh / the longest-idle lane.
+  int64_t big_lane_bytes = 0;  // measured worse (BERT 1.568 -> 1.610-1.648 ms)
+  // dataflow launch: persistent grids capped at this fraction of the
+  // resident CTA slots, so concurrent kernels co-reside instead of waiting
+  // for each other's CTAs to retire (1 = a full resident wave)
+  double grid_fraction = 1.0;  // measured neutral-to-worse (1.775 vs 1.783 ms at 4 lanes): opt-in
   int chunk_ring = 2;
   CodegenOptions codegen;
   // per fused-op codegen overrides {op id: {option: value}} (the measured
