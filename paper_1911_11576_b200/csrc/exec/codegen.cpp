@@ -833,6 +833,7 @@ bool Builder::plan_row(Component& c) {
     if (max_inner > 4096) nt = 512;
     if (max_inner > 8192) nt = 1024;
     if (forced_cta) nt = opts_.cta_rows;
+    if (!forced_cta && opts_.cta_threads > 0 && max_inner >= opts_.cta_threads) nt = opts_.cta_threads;
     // wide multi-gradient rows: a small CTA (2 warps for 768 columns) per
     // row -- ~12 columns per thread, cheap 64-thread barriers, many rows
     // in flight per SM

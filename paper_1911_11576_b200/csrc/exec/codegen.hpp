@@ -108,6 +108,10 @@ struct CodegenOptions {
   // warp per row (register-heavy multi-layer groups: more warps resident,
   // fewer values per thread); a per-group tuning candidate
   int cta_rows = 0;
+  // > 0: threads per row of CTA-row groups (default 256 up to 4096 elements):
+  // fewer elements per thread and more, smaller CTAs per SM -- a finer
+  // round-up tail over 4096 rows; a per-group tuning candidate
+  int cta_threads = 0;
   // Row-scheme inputs (body parameter ids) whose only reader is this kernel
   // and that are not graph outputs (arena intermediates): after a row is
   // consumed its 128-byte lines are invalidated in L2 (discard.global.L2),

@@ -115,6 +115,7 @@ void apply_codegen_options(CodegenOptions& c, const json::Value& o) {
   if (o.has("flat_elementwise")) c.flat_elementwise = o.at("flat_elementwise").as_bool();
   if (o.has("split_cross")) c.split_cross = o.at("split_cross").as_bool();
   if (o.has("cta_rows")) c.cta_rows = static_cast<int>(o.at("cta_rows").as_int());
+  if (o.has("cta_threads")) c.cta_threads = static_cast<int>(o.at("cta_threads").as_int());
   if (o.has("l2_discard")) c.l2_discard = o.at("l2_discard").as_bool();
   if (o.has("narrow_row_max")) c.narrow_row_max = static_cast<int>(o.at("narrow_row_max").as_int());
   if (o.has("rcp_divide")) c.rcp_divide = o.at("rcp_divide").as_bool();

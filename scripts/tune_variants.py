@@ -59,6 +59,10 @@ VARIANTS = [
     {"cta_rows": 192},
     {"cta_rows": 256},
     {"cta_rows": 192, "loop_fusion": False},
+    {"cta_threads": 128},
+    {"cta_threads": 384},
+    {"cta_threads": 512},
+    {"cta_threads": 768},
 ]
 # Not candidates: split_cross (one kernel + grid barrier instead of a row
 # kernel and its fold). Timed alone the single kernel wins, inside the

@@ -217,7 +217,8 @@ VARIANTS = [dict(pack_sequential=True), dict(loop_fusion=False), dict(row_prefet
             dict(gws=False), dict(gws=False, tma_double_buffer=True),
             dict(pdl=False), dict(fold_constants=False), dict(colred_cp_async=False), dict(colred_cols=128), dict(cross_smem=False), dict(tma_early=True),
             dict(split_cross=False), dict(narrow_rows=False), dict(cta_rows=192), dict(cta_rows=128),
-            dict(concurrent_lanes=1), dict(critical_priority=True), dict(flat_elementwise=True), dict(pdl_cooperative=False)]
+            dict(concurrent_lanes=1), dict(critical_priority=True), dict(flat_elementwise=True), dict(pdl_cooperative=False),
+            dict(cta_threads=384), dict(cta_threads=128), dict(l2_discard=False), dict(grid_fraction=0.5)]
 
 
 @pytest.mark.parametrize("name", list(W.CONFIGS))
