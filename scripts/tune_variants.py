@@ -63,6 +63,9 @@ VARIANTS = [
     {"cta_threads": 384},
     {"cta_threads": 512},
     {"cta_threads": 768},
+    {"cta_rows": 64},
+    {"cta_rows": 96},
+    {"cta_threads": 192},
 ]
 # Not candidates: split_cross (one kernel + grid barrier instead of a row
 # kernel and its fold). Timed alone the single kernel wins, inside the
