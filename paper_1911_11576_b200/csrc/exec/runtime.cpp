@@ -934,7 +934,17 @@ void Executor::launch_dag(const void* const* inputs, void* const* outputs, void*
   for (int k = 0; k < nk; ++k) {
     const std::vector<int>& pk = preds_[k];
     int lane = -1;
-    if (opts_.big_lane_bytes > 0 && nl > 1) {
+    if (opts_.fold_off_lane && kernels_[k].fold_of >= 0 && nl > 1) {
+      const int own = lane_of[kernels_[k].fold_of];
+      for (int l = 0; l < nl && lane < 0; ++l)
+        if (l != own && !used[l]) lane = l;
+      if (lane < 0) {
+        lane = own == 0 ? 1 : 0;
+        for (int l = 0; l < nl; ++l)
+          if (l != own && tail[l] < tail[lane]) lane = l;
+      }
+    }
+    if (lane < 0 && opts_.big_lane_bytes > 0 && nl > 1) {
       if (kernels_[k].spec.algo_bytes >= opts_.big_lane_bytes) {
         lane = 0;
       } else {

@@ -63,7 +63,10 @@ struct ExecOptions {
   // groups (parameter-gradient column reductions beside the activation-
   // gradient chain) fill each other's tails. <= 1: one stream in launch order.
   // Not used for chunked schedules or per-kernel profiling.
-  int concurrent_lanes = 3;  // measured: 3 lanes 1.739 ms, 4: 1.771, 8: 1.762, serial 2.003 (BERT step)
+  // measured (BERT step): serial 2.003 ms; before split folds 3 lanes 1.739,
+  // 4: 1.771, 8: 1.762; final executor 4 lanes + fold_off_lane 1.518 vs
+  // 3 lanes 1.553, 5: 1.544, 6: 1.545
+  int concurrent_lanes = 4;
   // dataflow launch: kernels on the estimated critical path (longest chain
   // of algorithmic bytes + per-launch overhead) launch at the highest
   // stream priority, so freed SM slots go to them before side branches
@@ -76,7 +79,10 @@ struct ExecOptions {
   // dataflow launch: persistent grids capped at this fraction of the
   // resident CTA slots, so concurrent kernels co-reside instead of waiting
   // for each other's CTAs to retire (1 = a full resident wave)
-  double grid_fraction = 1.0;  // measured neutral-to-worse (1.775 vs 1.783 ms at 4 lanes): opt-in
+  double grid_fraction = 1.0;
+  // a fold kernel goes to another lane than its row kernel (waiting on its
+  // event), so the row kernel's lane moves on without queueing behind it
+  bool fold_off_lane = true;  // measured neutral-to-worse (1.775 vs 1.783 ms at 4 lanes): opt-in
   int chunk_ring = 2;
   CodegenOptions codegen;
   // per fused-op codegen overrides {op id: {option: value}} (the measured
