@@ -679,6 +679,45 @@ void Executor::plan_deps() {
   for (int k = 0; k < nk; ++k) span = std::max(span, top[k] + bot[k]);
   critical_.assign(nk, false);
   for (int k = 0; k < nk; ++k) critical_[k] = top[k] + bot[k] >= 0.97 * span;
+  // issue order
+  issue_.clear();
+  {
+    std::vector<int> indeg(nk, 0);
+    std::vector<std::vector<int>> succ(nk);
+    for (int k = 0; k < nk; ++k)
+      for (int q : preds_[k]) {
+        ++indeg[k];
+        succ[q].push_back(k);
+      }
+    std::vector<int> ready;
+    for (int k = 0; k < nk; ++k)
+      if (!indeg[k]) ready.push_back(k);
+    bool big = true;
+    while (!ready.empty()) {
+      size_t pick = 0;
+      if (opts_.issue_order == 0) {
+        pick = std::min_element(ready.begin(), ready.end()) - ready.begin();
+      } else {
+        auto key = [&](int k) { return kernels_[k].fold_of >= 0 ? INT64_MAX : kernels_[k].spec.algo_bytes; };
+        bool fold = false;
+        for (size_t r = 0; r < ready.size() && !fold; ++r)
+          if (kernels_[ready[r]].fold_of >= 0) pick = r, fold = true;
+        if (!fold)
+          for (size_t r = 1; r < ready.size(); ++r) {
+            const bool better = (opts_.issue_order == 1 || big) ? key(ready[r]) > key(ready[pick])
+                                                                : key(ready[r]) < key(ready[pick]);
+            if (better || (key(ready[r]) == key(ready[pick]) && ready[r] < ready[pick])) pick = r;
+          }
+        if (!fold) big = !big;
+      }
+      const int k = ready[pick];
+      ready.erase(ready.begin() + static_cast<long>(pick));
+      issue_.push_back(k);
+      for (int q : succ[k])
+        if (--indeg[q] == 0) ready.push_back(q);
+    }
+    if (static_cast<int>(issue_.size()) != nk) throw InternalError("dataflow: dependency cycle");
+  }
   const size_t words = (static_cast<size_t>(nk) + 63) / 64;
   anc_.assign(nk, std::vector<uint64_t>(words, 0));
   for (int k = 0; k < nk; ++k)
@@ -928,11 +967,16 @@ void Executor::launch_dag(const void* const* inputs, void* const* outputs, void*
   auto ev = [&](int k) { return static_cast<CUevent>(dag_events_[k]); };
   CUevent fork = static_cast<CUevent>(dag_events_[nk]);
   cu_check(cu.cuEventRecord(fork, lane_stream(0)), "dag fork");
-  std::vector<int> tail(nl, -1), lane_of(nk, -1);
+  std::vector<int> tail(nl, -1), lane_of(nk, -1), pos(nk, -1);
   std::vector<bool> used(nl, false);
   used[0] = true;
-  for (int k = 0; k < nk; ++k) {
-    const std::vector<int>& pk = preds_[k];
+  for (int it = 0; it < nk; ++it) {
+    const int k = issue_[it];
+    pos[k] = it;
+    // latest-issued predecessor first (pk.back())
+    std::vector<int> pk = preds_[k];
+    std::sort(pk.begin(), pk.end(), [&](int a, int b) { return pos[a] < pos[b]; });
+    auto older = [&](int l, int m) { return (tail[l] < 0 ? -1 : pos[tail[l]]) < (tail[m] < 0 ? -1 : pos[tail[m]]); };
     int lane = -1;
     if (opts_.fold_off_lane && kernels_[k].fold_of >= 0 && nl > 1) {
       const int own = lane_of[kernels_[k].fold_of];
@@ -941,7 +985,7 @@ void Executor::launch_dag(const void* const* inputs, void* const* outputs, void*
       if (lane < 0) {
         lane = own == 0 ? 1 : 0;
         for (int l = 0; l < nl; ++l)
-          if (l != own && tail[l] < tail[lane]) lane = l;
+          if (l != own && older(l, lane)) lane = l;
       }
     }
     if (lane < 0 && opts_.big_lane_bytes > 0 && nl > 1) {
@@ -955,7 +999,7 @@ void Executor::launch_dag(const void* const* inputs, void* const* outputs, void*
         if (lane < 0) {
           lane = 1;
           for (int l = 2; l < nl; ++l)
-            if (tail[l] < tail[lane]) lane = l;
+            if (older(l, lane)) lane = l;
         }
       }
     }
@@ -967,7 +1011,7 @@ void Executor::launch_dag(const void* const* inputs, void* const* outputs, void*
     if (lane < 0) {
       lane = 0;
       for (int l = 1; l < nl; ++l)
-        if (tail[l] < tail[lane]) lane = l;
+        if (older(l, lane)) lane = l;
     }
     CUstream st = lane_stream(lane);
     if (!used[lane]) {
@@ -975,7 +1019,8 @@ void Executor::launch_dag(const void* const* inputs, void* const* outputs, void*
       used[lane] = true;
     }
     std::vector<int> latest(nl, -1);
-    for (int p : pk) latest[lane_of[p]] = std::max(latest[lane_of[p]], p);
+    for (int p : pk)
+      if (latest[lane_of[p]] < 0 || pos[p] > pos[latest[lane_of[p]]]) latest[lane_of[p]] = p;
     for (int l = 0; l < nl; ++l)
       if (l != lane && latest[l] >= 0) cu_check(cu.cuStreamWaitEvent(st, ev(latest[l]), 0), "dag wait");
     launch_one(k, 0, 1, inputs, outputs, st);
