@@ -66,6 +66,7 @@ int stitch_executor_create(const char* fused_graph_json, const char* options_jso
     if (o.has("grid_fraction")) opts.grid_fraction = o.at("grid_fraction").as_real();
     if (o.has("fold_off_lane")) opts.fold_off_lane = o.at("fold_off_lane").as_bool();
     if (o.has("issue_order")) opts.issue_order = static_cast<int>(o.at("issue_order").as_int());
+    if (o.has("pdl_true_deps_only")) opts.pdl_true_deps_only = o.at("pdl_true_deps_only").as_bool();
     if (o.has("fold_constants")) opts.fold_constants = o.at("fold_constants").as_bool();
     if (o.has("sink_broadcasts")) opts.sink_broadcasts = o.at("sink_broadcasts").as_bool();
     if (o.has("overlap_copies")) opts.overlap_copies = o.at("overlap_copies").as_bool();

@@ -936,7 +936,7 @@ void Executor::launch_one(int i, int c, int chunks, const void* const* inputs, v
     attr[na_attr].id = CU_LAUNCH_ATTRIBUTE_COOPERATIVE;
     attr[na_attr++].value.cooperative = 1;
   }
-  if (opts_.pdl && (!k.spec.cooperative || opts_.pdl_cooperative)) {
+  if (opts_.pdl && pdl_this_launch_ && (!k.spec.cooperative || opts_.pdl_cooperative)) {
     // overlap this launch with the previous kernel's tail (the kernel waits
     // in griddepcontrol.wait before reading anything)
     attr[na_attr].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
@@ -1023,7 +1023,10 @@ void Executor::launch_dag(const void* const* inputs, void* const* outputs, void*
       if (latest[lane_of[p]] < 0 || pos[p] > pos[latest[lane_of[p]]]) latest[lane_of[p]] = p;
     for (int l = 0; l < nl; ++l)
       if (l != lane && latest[l] >= 0) cu_check(cu.cuStreamWaitEvent(st, ev(latest[l]), 0), "dag wait");
+    pdl_this_launch_ = !opts_.pdl_true_deps_only || tail[lane] < 0 ||
+                       std::find(pk.begin(), pk.end(), tail[lane]) != pk.end();
     launch_one(k, 0, 1, inputs, outputs, st);
+    pdl_this_launch_ = true;
     cu_check(cu.cuEventRecord(ev(k), st), "dag done");
     tail[lane] = k;
     lane_of[k] = lane;

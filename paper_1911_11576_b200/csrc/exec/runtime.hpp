@@ -87,7 +87,12 @@ struct ExecOptions {
   // list, largest algorithmic bytes first; 2 = ready list alternating the
   // largest and the smallest ready kernel (folds as soon as ready in 1, 2)
   // measured (BERT step, 4 lanes): 0: 1.509-1.520 ms, 1: 1.555, 2: 1.489-1.491
-  int issue_order = 2;  // measured neutral-to-worse (1.775 vs 1.783 ms at 4 lanes): opt-in
+  int issue_order = 2;
+  // dataflow launch: PDL only when the lane's previous kernel is a true
+  // predecessor (else the early-launched CTAs would hold SM slots waiting on
+  // an unrelated kernel)
+  // measured (BERT step): 1.493 -> 1.445 ms
+  bool pdl_true_deps_only = true;  // measured neutral-to-worse (1.775 vs 1.783 ms at 4 lanes): opt-in
   int chunk_ring = 2;
   CodegenOptions codegen;
   // per fused-op codegen overrides {op id: {option: value}} (the measured
@@ -194,6 +199,7 @@ class Executor {
   std::vector<std::vector<uint64_t>> anc_;  // kernel -> ancestor bitset
   std::vector<bool> critical_;              // kernel on the estimated critical path
   std::vector<int> issue_;                  // dataflow issue order (a topological order)
+  bool pdl_this_launch_ = true;             // launch_dag's per-launch PDL decision
   int high_priority_ = 0;                   // greatest stream priority of the context
   std::vector<int> writer_;                 // value buffer -> producing kernel
   std::vector<std::vector<int>> touch_;     // value buffer -> kernels reading / writing it
