@@ -2735,7 +2735,7 @@ bool Builder::build_gws() {
        << ") {\n";
   head << "  extern __shared__ __align__(1024) unsigned char smem[];\n";
   head << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
-  head << "  asm volatile(\"griddepcontrol.launch_dependents;\");\n";
+  if (opts_.pdl_early_trigger) head << "  asm volatile(\"griddepcontrol.launch_dependents;\");\n";
   if (opts_.trace) head << "  stitch_dev::TraceScope stitch_trace_(gsync);\n";
   head << "  (void)ws; (void)gsync; (void)row_lo; (void)row_hi;\n";
   head << "  const Tail tail{";
@@ -2825,7 +2825,7 @@ bool Builder::build_gemm() {
   h << "extern \"C\" __global__ void __launch_bounds__(256) " << name_ << "(" << join(params, ", ") << ") {\n";
   h << "  extern __shared__ __align__(128) float smem[];\n";
   h << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
-  h << "  asm volatile(\"griddepcontrol.launch_dependents;\");\n";
+  if (opts_.pdl_early_trigger) h << "  asm volatile(\"griddepcontrol.launch_dependents;\");\n";
   if (opts_.trace) h << "  stitch_dev::TraceScope stitch_trace_(gsync);\n";
   h << "  (void)ws; (void)gsync; (void)row_lo; (void)row_hi;\n";
   h << "  stitch_dev::gemm::run<" << L(M) << ", " << L(N) << ", " << L(K) << ", " << L(batch) << ", " << L(sam) << ", "
@@ -3125,7 +3125,7 @@ KernelSpec Builder::build() {
   // global data, and let the next kernel get scheduled right away (our grids
   // are one resident wave, so its CTAs only take slots this one leaves free).
   head << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
-  head << "  asm volatile(\"griddepcontrol.launch_dependents;\");\n";
+  if (opts_.pdl_early_trigger) head << "  asm volatile(\"griddepcontrol.launch_dependents;\");\n";
   if (opts_.trace) head << "  stitch_dev::TraceScope stitch_trace_(gsync);\n";
   head << "  (void)ws; (void)gsync; (void)smem; (void)row_lo; (void)row_hi;\n";
   spec_.source = head.str() + body_src + "}\n";
@@ -3137,7 +3137,7 @@ KernelSpec Builder::build() {
     fh << "extern \"C\" __global__ void __launch_bounds__(256) " << spec_.fin_name << "(" << join(params, ", ") << ") {\n";
     fh << "  extern __shared__ __align__(128) float smem[];\n";
     fh << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
-    fh << "  asm volatile(\"griddepcontrol.launch_dependents;\");\n";
+    if (opts_.pdl_early_trigger) fh << "  asm volatile(\"griddepcontrol.launch_dependents;\");\n";
     if (opts_.trace) fh << "  stitch_dev::TraceScope stitch_trace_(gsync);\n";
     fh << "  (void)ws; (void)gsync; (void)smem; (void)row_lo; (void)row_hi;\n";
     spec_.fin_source = fh.str() + fin_body_ + "}\n";

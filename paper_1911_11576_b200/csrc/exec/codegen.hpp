@@ -118,7 +118,11 @@ struct CodegenOptions {
   // so dirty lines the producer left there are never written back to HBM.
   // Filled per kernel by the executor when `l2_discard` is on.
   std::set<std::string> discard_inputs;
-  bool l2_discard = true;  // measured worse (BERT 1.726 -> 1.773 ms): one 128-bit load per thread in flight
+  bool l2_discard = true;
+  // griddepcontrol.launch_dependents at kernel entry (a PDL dependent may be
+  // scheduled as soon as every CTA of this kernel runs); false: implicit at
+  // CTA exit
+  bool pdl_early_trigger = true;  // measured worse (BERT 1.726 -> 1.773 ms): one 128-bit load per thread in flight
   int narrow_row_max = 256;
   bool loop_fusion = true;
   bool colred = true;
