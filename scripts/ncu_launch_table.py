@@ -58,10 +58,14 @@ for cfg, kind, seq in seqs:
     out_md += ["## %s (%s, %d launches)" % (cfg, kind, len(seq)), "",
                "| kernel | us | DRAM read MB | DRAM write MB | L2 write MB | traffic MB |", "|---|---|---|---|---|---|"]
     tot = [0.0] * 5
+    # the dataflow launch issues in its own (topological) order: match this
+    # config's launches by name, list them in schedule order
+    chunk = ours[pos:pos + len(seq)]
+    pos += len(seq)
+    assert sorted(x["name"] for x in chunk) == sorted(seq), (cfg, kind)
+    by_name = {x["name"]: x for x in chunk}
     for name in seq:
-        L = ours[pos]
-        pos += 1
-        assert L["name"] == name, (L["name"], name)
+        L = by_name[name]
         us = L.get("gpu__time_duration.sum", 0)
         rd = L.get("dram__bytes_read.sum", 0)
         wr = L.get("dram__bytes_write.sum", 0)
