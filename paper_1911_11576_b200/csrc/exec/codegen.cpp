@@ -1324,6 +1324,8 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
   }
   ln("float* red = slab + " + std::to_string(c.slab_floats) + ";");
   ln("(void)red;");
+  const bool pp = c.cta && NT > 32 && opts_.pp_reduce;
+  if (pp) ln("int rpp = 0;  // in-row reductions alternate red[0..31] / red[64..95]");
   for (int v = 0; v < static_cast<int>(vals_.size()); ++v)
     if (c.staged[v] && !(c.dbuf && vals_[v].external))
       ln("float* sm" + std::to_string(v) + " = slab + " + std::to_string(c.smem_off[v]) + ";  // " + vals_[v].id);
@@ -1820,7 +1822,12 @@ void Builder::emit_row(Component& c, const std::string& lo, const std::string& n
         close();
         close();
         std::string s = fresh("s");
-        ln("const float " + s + " = stitch_dev::row_allreduce<" + std::to_string(NT) + ", " + Op + ">(" + acc + ", red);  // " + vals_[m].id);
+        if (c.cta && NT > 32 && opts_.pp_reduce) {
+          ln("const float " + s + " = stitch_dev::row_allreduce_pp<" + std::to_string(NT) + ", " + Op + ">(" + acc + ", red + 64 * rpp);  // " + vals_[m].id);
+          ln("rpp ^= 1;");
+        } else {
+          ln("const float " + s + " = stitch_dev::row_allreduce<" + std::to_string(NT) + ", " + Op + ">(" + acc + ", red);  // " + vals_[m].id);
+        }
         scalar_[m] = s;
       } else {
         // partial in-row reduce from the staged input tile
@@ -2917,7 +2924,13 @@ KernelSpec Builder::build() {
     spec_.max_grid = static_cast<int>(std::min<int64_t>((maxe + block - 1) / block, opts_.num_sms * 8));
   } else {
     // Workspace for cross-row partials: one row of partials per CTA.
-    const int64_t max_ctas = static_cast<int64_t>(opts_.num_sms) * 32;
+    // (resident CTAs: <= 2048 threads and <= 32 CTAs per SM; warp-row
+    // kernels may be launched with blocks down to 64 threads)
+    bool flex_rows = true;
+    for (const Component& c : comps) flex_rows = flex_rows && ((c.scheme == "row" && !c.cta) || c.scheme == "flat");
+    const int min_block = flex_rows ? 64 : block;
+    const int64_t max_ctas = static_cast<int64_t>(opts_.num_sms) * std::min(32, 2048 / std::max(32, min_block));
+    spec_.max_partials = static_cast<int>(max_ctas);
     bool coop = false;
     for (Component& c : comps)
       for (int x : c.cross) {
@@ -3007,7 +3020,7 @@ KernelSpec Builder::build() {
       if (c.scheme == "row") {
         emit_row(c, lo[i], n[i], "");
         rowc.push_back(&c);
-        smem_floats = std::max<int64_t>(smem_floats, c.cta ? c.slab_floats + 32 + 8 +
+        smem_floats = std::max<int64_t>(smem_floats, c.cta ? c.slab_floats + 32 + 8 + (opts_.pp_reduce ? 64 : 0) +
                                                                  (c.tc ? (c.tcp ? static_cast<int64_t>(c.tc_list.size()) : 1) *
                                                                                  int64_t{4} * 64 * c.tc_k + 64 * 68
                                                                        : 0)

@@ -68,6 +68,7 @@ struct KernelSpec {
   int64_t rows = 0;
   int rows_per_cta = 1;
   int row_threads = 32;  // threads per row of a single warp-row component (flex_block grids)
+  int max_partials = 0;  // > 0: the workspace holds this many per-CTA partial rows (grid cap)
   // split_cross: the fixed-order combine of the per-CTA column partials runs
   // as a second kernel `fin_name` (same arguments; row_lo = the partial count,
   // i.e. this kernel's grid) -- no grid barrier, so this kernel is not
@@ -122,7 +123,10 @@ struct CodegenOptions {
   // griddepcontrol.launch_dependents at kernel entry (a PDL dependent may be
   // scheduled as soon as every CTA of this kernel runs); false: implicit at
   // CTA exit
-  bool pdl_early_trigger = true;  // measured worse (BERT 1.726 -> 1.773 ms): one 128-bit load per thread in flight
+  bool pdl_early_trigger = true;
+  // CTA rows: in-row reductions alternate two scratch buffers, one CTA
+  // barrier per reduction instead of two
+  bool pp_reduce = false;  // measured neutral-to-worse on BERT (1.454 -> 1.469 ms): opt-in  // measured worse (BERT 1.726 -> 1.773 ms): one 128-bit load per thread in flight
   int narrow_row_max = 256;
   bool loop_fusion = true;
   bool colred = true;

@@ -118,6 +118,7 @@ void apply_codegen_options(CodegenOptions& c, const json::Value& o) {
   if (o.has("cta_threads")) c.cta_threads = static_cast<int>(o.at("cta_threads").as_int());
   if (o.has("l2_discard")) c.l2_discard = o.at("l2_discard").as_bool();
   if (o.has("pdl_early_trigger")) c.pdl_early_trigger = o.at("pdl_early_trigger").as_bool();
+  if (o.has("pp_reduce")) c.pp_reduce = o.at("pp_reduce").as_bool();
   if (o.has("narrow_row_max")) c.narrow_row_max = static_cast<int>(o.at("narrow_row_max").as_int());
   if (o.has("rcp_divide")) c.rcp_divide = o.at("rcp_divide").as_bool();
   if (o.has("trace")) c.trace = o.at("trace").as_bool();
@@ -813,6 +814,8 @@ void Executor::init_device() {
       throw std::runtime_error("kernel " + k.spec.name + ": packed components need " + std::to_string(k.spec.min_grid) +
                                " resident CTAs");
     if (k.spec.cooperative) k.grid = static_cast<int>(std::min<int64_t>(k.grid, static_cast<int64_t>(sms_) * 32));
+    if (k.spec.max_partials > 0 && k.spec.cluster == 0 && !k.spec.chunkable)
+      k.grid = std::min(k.grid, k.spec.max_partials);  // one workspace partial row per CTA
     if (k.spec.cluster > 0) {
       // cluster kernels map CTAs to work statically: exactly max_grid CTAs
       // (a multiple of the cluster size), clusters scheduled in waves
