@@ -1380,6 +1380,13 @@ json::Value Executor::describe() const {
     e.set("outputs", json::Value::array_of(k.spec.outputs));
     e.set("cache_hit", k.cache_hit);
     if (k.fold_of >= 0) e.set("fold_of", kernels_[k.fold_of].spec.name);
+    if (dag_) {
+      const size_t ki = static_cast<size_t>(&k - kernels_.data());
+      json::Value after = json::Value::array();
+      for (int q : preds_[ki]) after.push(kernels_[q].spec.name);
+      e.set("after", after);
+      e.set("issue_pos", static_cast<int64_t>(std::find(issue_.begin(), issue_.end(), static_cast<int>(ki)) - issue_.begin()));
+    }
     algo += k.spec.algo_bytes;
     ks.push(e);
   }
