@@ -3147,7 +3147,7 @@ KernelSpec Builder::build() {
     std::ostringstream fh;
     fh << "// column-reduction fold of fused op '" << name_ << "': fixed-order combine of the per-CTA partials "
        << name_ << " wrote to the workspace\n";
-    fh << "extern \"C\" __global__ void __launch_bounds__(256) " << spec_.fin_name << "(" << join(params, ", ") << ") {\n";
+    fh << "extern \"C\" __global__ void __launch_bounds__(1024) " << spec_.fin_name << "(" << join(params, ", ") << ") {\n";
     fh << "  extern __shared__ __align__(128) float smem[];\n";
     fh << "  asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
     if (opts_.pdl_early_trigger) fh << "  asm volatile(\"griddepcontrol.launch_dependents;\");\n";

@@ -394,11 +394,11 @@ void Executor::build_kernels() {
       f.spec.fin_source.clear();
       f.spec.scheme = "fold(" + std::to_string(k.spec.fin_outputs.size()) + " column reductions of " + k.spec.name + ")";
       f.spec.composition = {"block"};
-      f.spec.block = 256;
+      f.spec.block = opts_.fold_threads;
       f.spec.max_grid = k.spec.fin_max_grid;
       f.spec.min_grid = 1;
       f.spec.cooperative = false;
-      f.spec.smem_bytes = k.spec.fin_smem_bytes;
+      f.spec.smem_bytes = opts_.fold_threads * 4 + 16;
       f.spec.sync_words = 0;
       f.spec.chunkable = false;
       f.spec.flex_block = false;

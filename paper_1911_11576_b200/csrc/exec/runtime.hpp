@@ -92,7 +92,10 @@ struct ExecOptions {
   // predecessor (else the early-launched CTAs would hold SM slots waiting on
   // an unrelated kernel)
   // measured (BERT step): 1.493 -> 1.445 ms
-  bool pdl_true_deps_only = true;  // measured neutral-to-worse (1.775 vs 1.783 ms at 4 lanes): opt-in
+  bool pdl_true_deps_only = true;
+  // threads per CTA of the fold kernels (split_cross): blockDim / 32 slices
+  // of the partial rows per column block (the association follows it)
+  int fold_threads = 256;  // measured: 512 neutral, 1024 +1.7 % (BERT step)  // measured neutral-to-worse (1.775 vs 1.783 ms at 4 lanes): opt-in
   int chunk_ring = 2;
   CodegenOptions codegen;
   // per fused-op codegen overrides {op id: {option: value}} (the measured
