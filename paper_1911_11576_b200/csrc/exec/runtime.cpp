@@ -915,7 +915,11 @@ void Executor::launch_one(int i, int c, int chunks, const void* const* inputs, v
                                            3, reinterpret_cast<void*>(ptr), dims, strides, box, es,
                                            CU_TENSOR_MAP_INTERLEAVE_NONE,
                                            tp.swizzle ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
-                                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE),
+                                           opts_.tma_l2_promotion == 0   ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                                           : opts_.tma_l2_promotion == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                           : opts_.tma_l2_promotion == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                                                         : CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE),
                  "cuTensorMapEncodeTiled");
         k.tmap_ptrs[t] = ptr;
       }

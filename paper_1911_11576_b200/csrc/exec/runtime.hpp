@@ -95,6 +95,9 @@ struct ExecOptions {
   bool pdl_true_deps_only = true;
   // threads per CTA of the fold kernels (split_cross): blockDim / 32 slices
   // of the partial rows per column block (the association follows it)
+  // gws tensor maps: L2 promotion of the TMA tile reads (0 none, 1 64B,
+  // 2 128B, 3 256B)
+  int tma_l2_promotion = 3;
   int fold_threads = 256;  // measured: 512 neutral, 1024 +1.7 % (BERT step)  // measured neutral-to-worse (1.775 vs 1.783 ms at 4 lanes): opt-in
   int chunk_ring = 2;
   CodegenOptions codegen;

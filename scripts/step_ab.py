@@ -33,7 +33,10 @@ outs = [torch.empty(t["dims"], device="cuda") for t in exs[0].info["outputs"]]
 times = [[] for _ in variants]
 # round-robin: every variant measured in every round (drift hits all alike)
 for rnd in range(rounds):
-    for vi, ex in enumerate(exs):
+    # rotate the order every round: the variant measured first after a
+    # switch runs slower (seen as a ~2 us penalty on a 72 us kernel)
+    for vi in [(rnd + j) % len(exs) for j in range(len(exs))]:
+        ex = exs[vi]
         for it in range(8):
             with torch.cuda.stream(s):
                 flush.zero_()
