@@ -17,16 +17,20 @@ rounds = int(sys.argv[-1]) if not sys.argv[-1].endswith(".json") else 6
 torch.cuda.set_device(0)
 s = torch.cuda.Stream()
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+rd = torch.ones(64 << 20, device="cuda")  # read after the flush: no dirty lines left in L2
+sink = torch.empty((), device="cuda")
 fused = tuning.config_plan(name)[0]["fused"]
 exs = [rt.Executor(fused, kernel_options=json.load(open(f))["table"]) for f in files]
 ins = [torch.randn(t["dims"], device="cuda") for t in exs[0].info["inputs"]]
 outs = [torch.empty(t["dims"], device="cuda") for t in exs[0].info["outputs"]]
 times = [[] for _ in files]
-for _ in range(rounds):
-    for i, ex in enumerate(exs):
+for rnd in range(rounds):
+    for i in [(rnd + j) % len(exs) for j in range(len(exs))]:  # rotated: no first-after-switch bias
+        ex = exs[i]
         for it in range(8):
             with torch.cuda.stream(s):
                 flush.zero_()
+                torch.sum(rd, 0, out=sink)
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(s)
                 ex.run(ins, outs, stream=s.cuda_stream)

@@ -66,6 +66,11 @@ VARIANTS = [
     {"cta_rows": 64},
     {"cta_rows": 96},
     {"cta_threads": 192},
+    {"cta_rows": 192, "lazy_inputs": True},
+    {"cta_rows": 128, "lazy_inputs": True},
+    {"cta_rows": 256, "lazy_inputs": True},
+    {"cta_threads": 384, "lazy_inputs": True},
+    {"cta_rows": 192, "min_ctas_per_sm": 2},
 ]
 # Not candidates: split_cross (one kernel + grid barrier instead of a row
 # kernel and its fold). Timed alone the single kernel wins, inside the
