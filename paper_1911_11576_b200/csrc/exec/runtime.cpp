@@ -695,6 +695,7 @@ void Executor::plan_deps() {
     for (int k = 0; k < nk; ++k)
       if (!indeg[k]) ready.push_back(k);
     bool big = true;
+    int phase = 0;  // issue_order 3: two largest, then one smallest
     while (!ready.empty()) {
       size_t pick = 0;
       if (opts_.issue_order == 0) {
@@ -706,11 +707,14 @@ void Executor::plan_deps() {
           if (kernels_[ready[r]].fold_of >= 0) pick = r, fold = true;
         if (!fold)
           for (size_t r = 1; r < ready.size(); ++r) {
-            const bool better = (opts_.issue_order == 1 || big) ? key(ready[r]) > key(ready[pick])
-                                                                : key(ready[r]) < key(ready[pick]);
+            const bool big_now = opts_.issue_order == 1 || (opts_.issue_order == 3 ? (phase % 3) != 2 : big);
+            const bool better = big_now ? key(ready[r]) > key(ready[pick]) : key(ready[r]) < key(ready[pick]);
             if (better || (key(ready[r]) == key(ready[pick]) && ready[r] < ready[pick])) pick = r;
           }
-        if (!fold) big = !big;
+        if (!fold) {
+          big = !big;
+          ++phase;
+        }
       }
       const int k = ready[pick];
       ready.erase(ready.begin() + static_cast<long>(pick));

@@ -85,8 +85,10 @@ struct ExecOptions {
   bool fold_off_lane = true;
   // dataflow issue order: 0 = the fused graph's topological order; 1 = ready
   // list, largest algorithmic bytes first; 2 = ready list alternating the
-  // largest and the smallest ready kernel (folds as soon as ready in 1, 2)
-  // measured (BERT step, 4 lanes): 0: 1.509-1.520 ms, 1: 1.555, 2: 1.489-1.491
+  // largest and the smallest ready kernel; 3 = two largest then one
+  // smallest (folds as soon as ready in 1-3)
+  // measured (BERT step, 4 lanes): 0: 1.509-1.520 ms, 1: 1.555, 2: 1.489-1.491;
+  // with the final defaults 2: 1.448, 3: 1.504
   int issue_order = 2;
   // dataflow launch: PDL only when the lane's previous kernel is a true
   // predecessor (else the early-launched CTAs would hold SM slots waiting on
