@@ -2686,9 +2686,13 @@ bool Builder::build_gws() {
   row_hook_ = nullptr;
   nr_div_ = opts_.nr_divide;
   close();
-  for (int v : outputs_)
-    ln("*reinterpret_cast<float2*>(" + out_ptr(v) + " + off) = make_float2(o" + std::to_string(v) + "[0], o" +
-       std::to_string(v) + "[1]);");
+  for (int v : outputs_) {
+    const std::string val = "make_float2(o" + std::to_string(v) + "[0], o" + std::to_string(v) + "[1])";
+    if (opts_.gws_stream_stores)
+      ln("__stcs(reinterpret_cast<float2*>(" + out_ptr(v) + " + off), " + val + ");  // evict-first");
+    else
+      ln("*reinterpret_cast<float2*>(" + out_ptr(v) + " + off) = " + val + ";");
+  }
   close();
   close();
   --indent_;

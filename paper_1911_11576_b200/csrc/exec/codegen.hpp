@@ -126,7 +126,9 @@ struct CodegenOptions {
   bool pdl_early_trigger = true;
   // CTA rows: in-row reductions alternate two scratch buffers, one CTA
   // barrier per reduction instead of two
-  bool pp_reduce = false;  // measured neutral-to-worse on BERT (1.454 -> 1.469 ms): opt-in  // measured worse (BERT 1.726 -> 1.773 ms): one 128-bit load per thread in flight
+  bool pp_reduce = false;
+  // gws tail: evict-first (st.global.cs) stores of the outputs
+  bool gws_stream_stores = false;  // measured neutral-to-worse on BERT (1.454 -> 1.469 ms): opt-in  // measured worse (BERT 1.726 -> 1.773 ms): one 128-bit load per thread in flight
   int narrow_row_max = 256;
   bool loop_fusion = true;
   bool colred = true;

@@ -119,6 +119,7 @@ void apply_codegen_options(CodegenOptions& c, const json::Value& o) {
   if (o.has("l2_discard")) c.l2_discard = o.at("l2_discard").as_bool();
   if (o.has("pdl_early_trigger")) c.pdl_early_trigger = o.at("pdl_early_trigger").as_bool();
   if (o.has("pp_reduce")) c.pp_reduce = o.at("pp_reduce").as_bool();
+  if (o.has("gws_stream_stores")) c.gws_stream_stores = o.at("gws_stream_stores").as_bool();
   if (o.has("narrow_row_max")) c.narrow_row_max = static_cast<int>(o.at("narrow_row_max").as_int());
   if (o.has("rcp_divide")) c.rcp_divide = o.at("rcp_divide").as_bool();
   if (o.has("trace")) c.trace = o.at("trace").as_bool();
