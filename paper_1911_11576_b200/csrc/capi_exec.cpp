@@ -67,6 +67,7 @@ int stitch_executor_create(const char* fused_graph_json, const char* options_jso
     if (o.has("fold_off_lane")) opts.fold_off_lane = o.at("fold_off_lane").as_bool();
     if (o.has("issue_order")) opts.issue_order = static_cast<int>(o.at("issue_order").as_int());
     if (o.has("pdl_true_deps_only")) opts.pdl_true_deps_only = o.at("pdl_true_deps_only").as_bool();
+    if (o.has("pdl_low_priority")) opts.pdl_low_priority = o.at("pdl_low_priority").as_bool();
     if (o.has("tma_l2_promotion")) opts.tma_l2_promotion = static_cast<int>(o.at("tma_l2_promotion").as_int());
     if (o.has("fold_threads")) {
       opts.fold_threads = static_cast<int>(o.at("fold_threads").as_int());

@@ -941,7 +941,9 @@ void Executor::launch_one(int i, int c, int chunks, const void* const* inputs, v
   cfg.hStream = static_cast<CUstream>(stream);
   CUlaunchAttribute attr[4];
   unsigned na_attr = 0;
-  if (dag_ && opts_.critical_priority && critical_[i] && high_priority_ != 0) {
+  const bool pdl_launch = opts_.pdl && pdl_this_launch_ && (!k.spec.cooperative || opts_.pdl_cooperative);
+  if (dag_ && high_priority_ != 0 &&
+      ((opts_.critical_priority && critical_[i]) || (opts_.pdl_low_priority && !pdl_launch))) {
     attr[na_attr].id = CU_LAUNCH_ATTRIBUTE_PRIORITY;
     attr[na_attr++].value.priority = high_priority_;
   }
@@ -949,7 +951,7 @@ void Executor::launch_one(int i, int c, int chunks, const void* const* inputs, v
     attr[na_attr].id = CU_LAUNCH_ATTRIBUTE_COOPERATIVE;
     attr[na_attr++].value.cooperative = 1;
   }
-  if (opts_.pdl && pdl_this_launch_ && (!k.spec.cooperative || opts_.pdl_cooperative)) {
+  if (pdl_launch) {
     // overlap this launch with the previous kernel's tail (the kernel waits
     // in griddepcontrol.wait before reading anything)
     attr[na_attr].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;

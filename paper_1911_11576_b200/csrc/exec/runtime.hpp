@@ -100,7 +100,11 @@ struct ExecOptions {
   // gws tensor maps: L2 promotion of the TMA tile reads (0 none, 1 64B,
   // 2 128B, 3 256B)
   int tma_l2_promotion = 3;
-  int fold_threads = 256;  // measured: 512 neutral, 1024 +1.7 % (BERT step)  // measured neutral-to-worse (1.775 vs 1.783 ms at 4 lanes): opt-in
+  int fold_threads = 256;
+  // dataflow launch: kernels launched without PDL get the highest stream
+  // priority, so CTA slots freed by a draining kernel go to runnable work
+  // before the early-launched (waiting) CTAs of its PDL dependent
+  bool pdl_low_priority = false;  // measured neutral (BERT 1.452 vs 1.453 ms)  // measured: 512 neutral, 1024 +1.7 % (BERT step)  // measured neutral-to-worse (1.775 vs 1.783 ms at 4 lanes): opt-in
   int chunk_ring = 2;
   CodegenOptions codegen;
   // per fused-op codegen overrides {op id: {option: value}} (the measured
