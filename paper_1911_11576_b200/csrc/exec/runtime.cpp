@@ -702,9 +702,11 @@ void Executor::plan_deps() {
       if (opts_.issue_order == 0) {
         pick = std::min_element(ready.begin(), ready.end()) - ready.begin();
       } else {
-        auto key = [&](int k) { return kernels_[k].fold_of >= 0 ? INT64_MAX : kernels_[k].spec.algo_bytes; };
+        auto key = [&](int k) {
+          return kernels_[k].fold_of >= 0 && opts_.issue_order != 4 ? INT64_MAX : kernels_[k].spec.algo_bytes;
+        };
         bool fold = false;
-        for (size_t r = 0; r < ready.size() && !fold; ++r)
+        for (size_t r = 0; r < ready.size() && !fold && opts_.issue_order != 4; ++r)
           if (kernels_[ready[r]].fold_of >= 0) pick = r, fold = true;
         if (!fold)
           for (size_t r = 1; r < ready.size(); ++r) {

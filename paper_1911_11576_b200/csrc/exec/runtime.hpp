@@ -86,9 +86,10 @@ struct ExecOptions {
   // dataflow issue order: 0 = the fused graph's topological order; 1 = ready
   // list, largest algorithmic bytes first; 2 = ready list alternating the
   // largest and the smallest ready kernel; 3 = two largest then one
-  // smallest (folds as soon as ready in 1-3)
+  // smallest (folds as soon as ready in 1-3); 4 = as 2 with folds ranked by
+  // their (zero) algorithmic bytes like any other kernel
   // measured (BERT step, 4 lanes): 0: 1.509-1.520 ms, 1: 1.555, 2: 1.489-1.491;
-  // with the final defaults 2: 1.448, 3: 1.504
+  // with the final defaults 2: 1.448, 3: 1.504, 4: 1.464
   int issue_order = 2;
   // dataflow launch: PDL only when the lane's previous kernel is a true
   // predecessor (else the early-launched CTAs would hold SM slots waiting on
